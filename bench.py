@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: PSA alias-table build + bulk alias sampling.
+
+Workload (BASELINE.json configs[1]): n = 1e8 float64 weights, Uniform(0,1]
+from the reference generator with seed 42, resident in HBM; one step =
+  (1) a full PSA build over them (K0 total, K1 partition, K2a/b/c compensated
+      block scans, K3 split searches, K4 pack -> 16-B buckets), then
+  (2) k = 1e9 with-replacement draws (K5) into a device buffer.
+value = (n + k) / step time, in G(items+samples)/s, whole job.  The two
+halves are reported separately under "build" and "sample" with their own
+rooflines.  N > 1 (torchrun): weak scaling -- every rank owns a contiguous
+shard of N*1e8 items, builds it, all-gathers the shard totals (NCCL), derives
+its sample count from the communication-free binomial split and draws it.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, i.e.
+the unmodified /root/reference headers; the C restatement when that build is
+absent) on this host's cores, same metric and config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ITEMS = 10**8
+K_SAMPLES = 10**9
+SEED = 42
+METRIC = "alias build Gitems/s + sample Gsamples/s at 1/2/4/8 B200; % HBM roofline"
+UNIT = "G(items+samples)/s"
+BUILD_BYTES_PER_ITEM = 80   # K0 8 + K1 20 + K2 24 + K4 28
+SAMPLE_BYTES_PER_DRAW = 36  # one 32-B sector gather + one 4-B index store
+KERNELS_PER_STEP = 8        # k_total, k_partition, k_scan_blocks x2, k_scan_carry,
+                            # k_split, k_pack, k_sample
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_ITEMS, help="items per GPU")
+    ap.add_argument("--k", type=int, default=K_SAMPLES, help="draws per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_per_unit():
+    """dram bytes per unit (item / sample) from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------- CPU arm
+def cpu_reference_step(n: int, k: int, k_sample: int, threads: int, w=None):
+    """One bounded sample of the workload on the host: the reference's
+    AliasTable(wt, psa, T) over n items (full size) and sample_many with T
+    threads over k_sample draws, extrapolated linearly to k draws.  Returns
+    (seconds for n + k, detail dict)."""
+    import numpy as np
+    import oracle
+    R = oracle.ref()
+    kind = "reference" if R is not None else "port"
+    if w is None:
+        w = (R or oracle.port()).generate_uniform(n, SEED)
+    if R is not None:
+        t0 = time.perf_counter()
+        table = R.table(w, threads)  # AliasTable(wt, psa, T): includes bucket alloc
+        t1 = time.perf_counter()
+        ob = R.lib.ref_outbuf_new(k_sample)
+        R.lib.ref_table_sample_into(table.h, SEED, k_sample, threads, ob)  # warm pages
+        t2 = time.perf_counter()
+        R.lib.ref_table_sample_into(table.h, SEED + 1, k_sample, threads, ob)
+        t3 = time.perf_counter()
+        R.lib.ref_outbuf_free(ob)
+        del table
+        cores = threads
+    else:
+        P = oracle.port()
+        t0 = time.perf_counter()
+        b, wn = P.psa_build(w, threads)
+        t1 = time.perf_counter()
+        out = np.empty(k_sample, np.uint32)
+        t2 = time.perf_counter()
+        P.lib.wo_sample_many(b.ctypes.data, n, wn, SEED, k_sample, 1, out.ctypes.data)
+        t3 = time.perf_counter()
+        cores = 1
+    t_build = t1 - t0
+    t_draw = (t3 - t2) * (k / k_sample)
+    return t_build + t_draw, {"kind": kind, "cores": cores, "build_s": t_build,
+                              "draw_s_per_1e9": (t3 - t2) * (1e9 / k_sample), "w": w}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # torchrun N>1: rank 0 alone runs the CPU arm
+    threads = os.cpu_count() or 1
+    n, k = args.n, args.k
+    k_sample = min(k, 10**8)
+    import oracle
+    oracle.build() if not os.path.exists(oracle.PORT_SO) else None
+    w = None
+    times = []
+    detail = {}
+    for i in range(args.warmup + args.steps):
+        t, detail = cpu_reference_step(n, k, k_sample, threads, w)
+        w = detail.pop("w")
+        if i >= args.warmup:
+            times.append(t)
+    sec = statistics.median(times)
+    value = (n + k) / sec / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generate_uniform(n, 42)",
+        "config": {"workload": "BASELINE configs[1]: n=1e8 uniform(0,1] f64, psa build + 1e9 draws",
+                   "n": n, "k": k},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": detail["cores"],
+                         "kind": detail["kind"],
+                         "sample": f"AliasTable(wt, psa, {threads}) over n={n} (median of "
+                                   f"{args.steps}) + sample_many({threads} threads) over "
+                                   f"{k_sample} draws extrapolated to k={k}",
+                         "build_s": detail["build_s"],
+                         "draw_s_per_1e9": detail["draw_s_per_1e9"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1903_00227_b200 as wrs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+
+    n_total, k_total = args.n * world, args.k * world
+    lo, hi = wrs.shard_range(n_total, world, rank)
+    W = wrs.Weights.generate_range("uniform", 0.0, n_total, lo, hi, SEED)
+    S = wrs.Sampler.build(W, "psa", 1)
+    n_local = hi - lo
+    out = torch.empty(int(args.k * 1.2) + 1024 if world > 1 else args.k, dtype=torch.int32,
+                      device=dev)
+    tot = torch.zeros(world, dtype=torch.float64, device=dev)
+    mine = torch.tensor([W.total()], dtype=torch.float64, device=dev)
+
+    def step(ev=None):
+        with torch.cuda.stream(stream):
+            if ev:
+                ev[0].record(stream)
+            S.rebuild_async(stream)
+            if ev:
+                ev[1].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(tot, mine)
+                counts = wrs.shard_counts(tot.cpu().numpy(), SEED, k_total)
+                k_me = int(counts[rank])
+                S.draw_shard_device(SEED, rank, k_me, lo, out, stream)
+            else:
+                k_me = args.k
+                S.draw_device(SEED, k_me, 1, out, stream)
+            if ev:
+                ev[2].record(stream)
+        return k_me
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    S.check()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    k_drawn = 0
+    with ClockSampler(local) as clocks:
+        t0.record(stream)
+        for i in range(args.steps):
+            k_drawn += step(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    S.check()
+    ms = t0.elapsed_time(t1)
+    build_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    draw_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    ms_step = ms / args.steps
+    if world > 1:
+        m = torch.tensor([ms_step, build_ms, draw_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        ms_step, build_ms, draw_ms = m.tolist()
+
+    hbm, hbm_kind = peaks()
+    k_per_rank = k_total / world
+    value = (n_total + k_total) / (ms_step * 1e-3) / 1e9
+    build_gbs = BUILD_BYTES_PER_ITEM * n_local / (build_ms * 1e-3) / 1e9
+    draw_gbs = SAMPLE_BYTES_PER_DRAW * k_per_rank / (draw_ms * 1e-3) / 1e9
+    tr = traffic_per_unit()
+
+    def traffic(key, units):
+        v = tr.get(key)
+        return None if v is None else v * units
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generate_uniform(n_total, 42) generated on device",
+        "config": {"workload": "BASELINE configs[1]: n=1e8 uniform(0,1] f64 per GPU, psa build "
+                               "+ 1e9 with-replacement draws per GPU",
+                   "n_per_gpu": args.n, "k_per_gpu": args.k, "jobs": S.jobs,
+                   "parallelism": f"shard{world}" if world > 1 else "single",
+                   "l2": "no flush: weights 0.8 GB, table 1.6 GB, output 4 GB > 126 MB L2"},
+        "build": {"gitems_per_s": n_local / (build_ms * 1e-3) / 1e9, "ms": build_ms,
+                  "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": hbm,
+                               "peak_kind": hbm_kind, "unit": "GB/s", "frac": build_gbs / hbm,
+                               "bytes_per_item": BUILD_BYTES_PER_ITEM}},
+        "sample": {"gsamples_per_s": k_per_rank / (draw_ms * 1e-3) / 1e9, "ms": draw_ms},
+        "roofline": {"bound": "hbm", "kernel": "k_sample", "achieved": draw_gbs, "peak": hbm,
+                     "peak_kind": hbm_kind, "unit": "GB/s", "frac": draw_gbs / hbm,
+                     "bytes_per_sample": SAMPLE_BYTES_PER_DRAW,
+                     "traffic": traffic("k_sample_bytes_per_sample", k_per_rank)},
+        "gpu_launches": KERNELS_PER_STEP * args.steps,
+        "clocks": clocks.summary(),
+    }
+
+    # ---- end to end through the C ABI with host buffers ---------------------
+    if not args.no_e2e:
+        result["e2e"] = e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total)
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        t, d = cpu_reference_step(args.n, args.k, min(args.k, 10**8), os.cpu_count() or 1)
+        result["cpu_baseline"] = {
+            "value": (args.n + args.k) / t / 1e9, "unit": UNIT, "cores": d["cores"],
+            "kind": d["kind"],
+            "sample": f"AliasTable(wt, psa, {d['cores']}) over n={args.n} + sample_many over "
+                      f"1e8 draws extrapolated to k={args.k}",
+            "build_s": d["build_s"], "draw_s_per_1e9": d["draw_s_per_1e9"]}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):
+    """wrs_weights_from_array(host) -> wrs_sampler_build("psa") ->
+    wrs_sampler_draw(host out): every step copies the weights H2D and the
+    draws D2H (pinned host memory), allocations included."""
+    import numpy as np
+    n = hi - lo
+    Wd = wrs.Weights.generate_range("uniform", 0.0, n_total, lo, hi, SEED)
+    host_w = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host_w.numpy()[:] = Wd.values()
+    Wd.free()
+    k = args.k
+    host_out = torch.empty(k, dtype=torch.int32, pin_memory=True)
+    steps = max(1, min(args.steps, 3))
+    times = []
+    for i in range(1 + steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        W = wrs.Weights.from_array(host_w.numpy())
+        S = wrs.Sampler.build(W, "psa", 1)
+        S.draw_into(SEED, k, 1, host_out.data_ptr())
+        checksum = int(host_out[-1])  # the step's result read on the host
+        t1 = time.perf_counter()
+        S.free()
+        W.free()
+        if i:
+            times.append(t1 - t0)
+    sec = statistics.median(times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    return {"value": (n_total + k * world) / sec / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * k, "ms_per_step": sec * 1e3,
+            "api": "wrs_weights_from_array + wrs_sampler_build(psa) + wrs_sampler_draw",
+            "checksum_last": checksum}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,113 @@
+/*
+ * include/wrs_b200.h -- B200 extensions to the wrs.h ABI (libwrs_b200.so).
+ *
+ * Everything here is additive: a reference client never needs it.  It exposes
+ * what a GPU caller wants beyond the reference surface -- device-resident
+ * input and output (so a 4 GB draw need not round-trip through the host), an
+ * explicit PSA job count, asynchronous rebuild/draw on a caller stream for
+ * timing, the sharded multi-GPU pieces, and read-back of the table and of the
+ * build's intermediate arrays for parity tests.  Plain pointers and sizes
+ * only; streams are passed as void* (a cudaStream_t, NULL = the handle's own).
+ */
+#ifndef WRS_B200_H
+#define WRS_B200_H
+
+#include "wrs.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* PSA job count "psa" uses for n items.  The table depends on it
+ * (alias.hpp:211-213 keeps only masses invariant), so parity tests run the
+ * reference at this same count. */
+WRS_API uint64_t wrs_b200_default_jobs(uint64_t n);
+
+/* Weights already in device memory of the current CUDA device.  copy != 0
+ * duplicates them; copy == 0 borrows d_w (caller keeps it alive and
+ * unchanged until every handle built from it is freed). */
+WRS_API wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
+                                                wrs_weights** out);
+/* Items [lo, hi) of the global vector wrs_weights_generate(dist, param,
+ * n_total, seed) would produce, generated directly on the device (a shard's
+ * slice).  Only "uniform" (counter-based) is supported per range. */
+WRS_API wrs_status wrs_b200_weights_generate_range(const char* dist, double param,
+                                                   uint64_t n_total, uint64_t lo, uint64_t hi,
+                                                   uint64_t seed, wrs_weights** out);
+/* Pairwise total W (weights.hpp:19-28, bit-exact) and the device pointer. */
+WRS_API double wrs_b200_weights_total(const wrs_weights* w);
+WRS_API const double* wrs_b200_weights_device(const wrs_weights* w);
+
+/* Build flags. */
+#define WRS_B200_KEEP_WORKSPACE 1u /* keep intermediates for wrs_b200_sampler_stage */
+
+/* PSA build with an explicit job count (0 = wrs_b200_default_jobs(n)). */
+WRS_API wrs_status wrs_b200_sampler_build_psa(const wrs_weights* w, uint64_t jobs,
+                                              unsigned flags, wrs_sampler** out);
+WRS_API uint64_t wrs_b200_sampler_jobs(const wrs_sampler* s);
+WRS_API uint64_t wrs_b200_sampler_size(const wrs_sampler* s);
+WRS_API double wrs_b200_sampler_bucket_mean(const wrs_sampler* s);
+WRS_API double wrs_b200_sampler_total(const wrs_sampler* s);
+/* Table as 16-byte {double share; uint32 item; uint32 alias} records
+ * (alias.hpp:26-33 byte layout). */
+WRS_API const void* wrs_b200_sampler_device_buckets(const wrs_sampler* s);
+WRS_API wrs_status wrs_b200_sampler_copy_buckets(const wrs_sampler* s, void* host_out);
+
+/* Re-run the whole build (K0..K4) in place from the sampler's weights,
+ * asynchronously on `stream`; no host synchronisation.  Plan errors are
+ * latched on the device and reported by wrs_b200_sampler_check. */
+WRS_API wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream);
+WRS_API wrs_status wrs_b200_sampler_check(const wrs_sampler* s);
+
+/* Draw into device memory, asynchronously on `stream`.  Same values as
+ * wrs_sampler_draw(s, seed, count, workers, ...). */
+WRS_API wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t seed,
+                                                uint64_t count, unsigned workers,
+                                                uint32_t* d_out, void* stream);
+
+/* Copy a named intermediate of the last build (needs WRS_B200_KEEP_WORKSPACE):
+ * "counts" (u64 nl, nh), "light", "heavy" (u32), "light_w", "heavy_w" (f64),
+ * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries), "block_totals",
+ * "carries" (f64, light blocks then heavy blocks), "split_light",
+ * "split_heavy" (u32, P + 1), "split_spill" (f64, P + 1).  *bytes receives
+ * the size; host_out may be NULL to query it. */
+WRS_API wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name,
+                                          void* host_out, uint64_t capacity,
+                                          uint64_t* bytes);
+
+/* Device time of each build stage of the last wrs_b200_sampler_rebuild_async
+ * made with timing on (wrs_b200_set_timing(1)), in milliseconds:
+ * [K0 total, K1 partition, K2a block totals, K2b carries, K2c prefixes,
+ *  K3 splits, K4 pack].  Returns the number written. */
+WRS_API int wrs_b200_set_timing(int on);
+WRS_API int wrs_b200_sampler_stage_times(const wrs_sampler* s, float* ms, int max);
+
+/* ---------------------------------------------------- sharded (multi-GPU)
+ * Contiguous shards of ceil(n/G) items (two_level.hpp:33-41).  Each rank
+ * builds its shard with "psa" and contributes the shard total; the top table
+ * over the G totals is built redundantly on every rank (two_level.hpp:56-57)
+ * and k is split across shards by a binomial descent that every rank
+ * reproduces from the seed (no communication).  The exchange of the G totals
+ * is done by the caller's collective (NCCL allgather of G doubles). */
+WRS_API void wrs_b200_shard_range(uint64_t n, uint64_t groups, uint64_t g,
+                                  uint64_t* lo, uint64_t* hi);
+/* counts[0..G) summing to k: sample counts per shard for (seed, k).  Pure
+ * host arithmetic, identical on every rank (binomial.hpp:161-170). */
+WRS_API wrs_status wrs_b200_shard_counts(const double* totals, uint64_t groups,
+                                         uint64_t seed, uint64_t k, uint64_t* counts);
+/* Seed shard g draws with: RngStream(seed, 'sdrw').derive(g) key. */
+WRS_API uint64_t wrs_b200_shard_seed(uint64_t seed, uint64_t shard);
+/* Draw `count` samples from shard `shard`'s table -- exactly
+ * AliasTable(shard).sample_many(wrs_b200_shard_seed(seed, shard), count, 1)
+ * -- and add `base` (the shard's first global id) to every index, into device
+ * memory, asynchronously on `stream`. */
+WRS_API wrs_status wrs_b200_sampler_draw_shard_device(const wrs_sampler* s, uint64_t seed,
+                                                      uint64_t shard, uint64_t count,
+                                                      uint64_t base, uint32_t* d_out,
+                                                      void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* WRS_B200_H */

@@ -1,0 +1,757 @@
+// paper_1903_00227_b200/csrc/capi.cpp -- the C ABI of include/wrs.h and
+// include/wrs_b200.h on top of the sm_100a kernels.
+//
+// Mirrors the reference's ABI conventions (capi.cpp:53-75 in the reference):
+// every call returns a wrs_status, exceptions never cross the boundary, the
+// failure text is kept per thread for wrs_last_error().  CUDA failures map to
+// WRS_ENOMEM (allocation) or WRS_EINTERNAL.  There is no CPU compute path:
+// a missing or unusable GPU makes every compute call fail loudly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "wrs.h"
+#include "wrs_b200.h"
+
+namespace {
+
+using wrsb::Bucket;
+
+// ---- error plumbing ----------------------------------------------------------
+struct io_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct format_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+    cudaError_t code;
+    cuda_error(cudaError_t c, const std::string& what)
+        : std::runtime_error(what + ": " + cudaGetErrorString(c)), code(c) {}
+};
+
+thread_local std::string t_last_error = "no error";
+
+wrs_status fail(wrs_status code, std::string msg) {
+    t_last_error = std::move(msg);
+    return code;
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear sticky-free errors
+        throw cuda_error(e, what);
+    }
+}
+
+template <typename F>
+wrs_status guarded(F&& f) {
+    try {
+        return f();
+    } catch (const std::bad_alloc&) {
+        return fail(WRS_ENOMEM, "out of memory");
+    } catch (const cuda_error& e) {
+        return fail(e.code == cudaErrorMemoryAllocation ? WRS_ENOMEM : WRS_EINTERNAL, e.what());
+    } catch (const format_error& e) {
+        return fail(WRS_EFORMAT, e.what());
+    } catch (const io_error& e) {
+        return fail(WRS_EIO, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(WRS_EINVAL, e.what());
+    } catch (const std::exception& e) {
+        return fail(WRS_EINTERNAL, e.what());
+    }
+}
+
+std::atomic<int> g_timing{0};
+
+// ---- device buffers ------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    DevBuf() = default;
+    explicit DevBuf(size_t bytes) { ck(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() { ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate"); }
+    ~Stream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+int current_device() {
+    int d = 0;
+    ck(cudaGetDevice(&d), "cudaGetDevice");
+    return d;
+}
+
+// Validated weights resident in HBM (weights.hpp:30-64 semantics).
+struct WeightsData {
+    int device = 0;
+    uint64_t n = 0;
+    double* d_w = nullptr;
+    bool owned = true;
+    double total = 0.0;
+    std::unique_ptr<DevBuf> storage;
+    mutable std::mutex host_mu;
+    mutable std::vector<double> host;  // lazily materialised values()
+    mutable bool host_ready = false;
+
+    const double* host_values() const {
+        std::lock_guard<std::mutex> g(host_mu);
+        if (!host_ready) {
+            host.resize(n);
+            ck(cudaSetDevice(device), "cudaSetDevice");
+            ck(cudaMemcpy(host.data(), d_w, n * sizeof(double), cudaMemcpyDeviceToHost),
+               "weights D2H");
+            host_ready = true;
+        }
+        return host.data();
+    }
+};
+
+// K0 on the device: validation + pairwise total; throws the reference's
+// exception for a bad weight (weights.hpp:38-41 / weight_file.hpp:94-96).
+void finalize_weights(WeightsData& wd, const std::string& file_for_format_error) {
+    if (wd.n == 0) throw std::invalid_argument("weights: need at least one item");
+    wrsb::Workspace ws;
+    ck(wrsb::workspace_alloc_total(ws, wd.n), "workspace");
+    struct Guard {
+        wrsb::Workspace& w;
+        ~Guard() { wrsb::workspace_free(w); }
+    } guard{ws};
+    Stream st;
+    ck(wrsb::launch_total(wd.d_w, wd.n, ws, st.s), "K0 launch");
+    wrsb::DevScalars sc{};
+    ck(cudaMemcpyAsync(&sc, ws.sc, sizeof sc, cudaMemcpyDeviceToHost, st.s), "scalars D2H");
+    ck(cudaStreamSynchronize(st.s), "K0");
+    if (sc.bad_index != ~0ull) {
+        if (!file_for_format_error.empty())
+            throw format_error("weight " + std::to_string(sc.bad_index) +
+                               " not finite/positive: " + file_for_format_error);
+        throw std::invalid_argument("weights: item " + std::to_string(sc.bad_index) +
+                                    " is not finite and positive");
+    }
+    wd.total = sc.total;
+}
+
+std::shared_ptr<WeightsData> weights_from_host(const double* w, uint64_t n,
+                                               const std::string& file = "") {
+    auto wd = std::make_shared<WeightsData>();
+    wd->device = current_device();
+    wd->n = n;
+    if (n == 0) throw std::invalid_argument("weights: need at least one item");
+    wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
+    wd->d_w = static_cast<double*>(wd->storage->p);
+    ck(cudaMemcpy(wd->d_w, w, n * sizeof(double), cudaMemcpyHostToDevice), "weights H2D");
+    finalize_weights(*wd, file);
+    return wd;
+}
+
+// Power-law weights (weight_file.hpp:42-54): (i+1)^-s in order, then the
+// reference's Fisher-Yates with RngStream(seed, 'genp').bounded(i).  The
+// shuffle is inherently sequential, so it runs once on the host as input
+// preparation; the result is uploaded and never recomputed.
+std::vector<double> powerlaw_host(uint64_t n, double s, uint64_t seed) {
+    if (!(s >= 0.0) || !std::isfinite(s))
+        throw std::invalid_argument("power law exponent must be finite and >= 0");
+    std::vector<double> w(n);
+    for (uint64_t i = 0; i < n; ++i) w[i] = std::pow(static_cast<double>(i + 1), -s);
+    const uint64_t key = wrsb::rng_key(seed, 0x67656e70u);
+    uint64_t ctr = 0;
+    for (uint64_t i = n; i > 1; --i) {
+        ctr += wrsb::kGolden;
+        const uint64_t r = wrsb::mix64(key + ctr);
+        const uint64_t j = static_cast<uint64_t>((static_cast<unsigned __int128>(r) * i) >> 64);
+        std::swap(w[i - 1], w[j]);
+    }
+    return w;
+}
+
+}  // namespace
+
+struct wrs_weights {
+    std::shared_ptr<WeightsData> data;
+};
+
+struct wrs_sampler {
+    std::shared_ptr<WeightsData> weights;  // retained for verification (capi.cpp:42)
+    std::string algo;
+    int device = 0;
+    uint64_t n = 0, P = 1;
+    double total = 0.0, wn = 0.0;
+    std::unique_ptr<DevBuf> buckets;
+    std::unique_ptr<Stream> stream;
+    wrsb::Workspace ws;
+    bool keep_ws = false;
+    cudaEvent_t ev[8] = {};
+    bool timed = false;
+    std::mutex mu;  // rebuild / stage access
+
+    ~wrs_sampler() {
+        if (device >= 0) cudaSetDevice(device);
+        wrsb::workspace_free(ws);
+        for (cudaEvent_t& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+    Bucket* d_b() const { return static_cast<Bucket*>(buckets->p); }
+};
+
+namespace {
+
+void read_scalars(wrs_sampler& s) {
+    wrsb::DevScalars sc{};
+    ck(cudaMemcpyAsync(&sc, s.ws.sc, sizeof sc, cudaMemcpyDeviceToHost, s.stream->s),
+       "scalars D2H");
+    ck(cudaStreamSynchronize(s.stream->s), "PSA build");
+    if (sc.plan_error) throw std::logic_error("alias split boundaries must be nondecreasing");
+    s.total = sc.total;
+    s.wn = sc.wn;
+}
+
+std::unique_ptr<wrs_sampler> build_psa(const std::shared_ptr<WeightsData>& wd, uint64_t P,
+                                       unsigned flags, const char* algo) {
+    if (wd->n > std::numeric_limits<uint32_t>::max())
+        throw std::invalid_argument("alias table limited to 2^32-1 items");
+    ck(cudaSetDevice(wd->device), "cudaSetDevice");
+    auto s = std::make_unique<wrs_sampler>();
+    s->weights = wd;
+    s->algo = algo;
+    s->device = wd->device;
+    s->n = wd->n;
+    s->P = P ? P : 1;
+    s->keep_ws = flags & WRS_B200_KEEP_WORKSPACE;
+    s->buckets = std::make_unique<DevBuf>(wd->n * sizeof(Bucket));
+    s->stream = std::make_unique<Stream>();
+    ck(wrsb::workspace_alloc(s->ws, s->n, s->P), "workspace");
+    ck(wrsb::launch_psa_build(wd->d_w, s->n, s->P, s->d_b(), s->ws, s->stream->s, nullptr),
+       "PSA launch");
+    read_scalars(*s);
+    if (!s->keep_ws) wrsb::workspace_free(s->ws);
+    return s;
+}
+
+bool is_device_pointer(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Draw positions [0, count) to a host buffer: chunks are drawn into two device
+// buffers and copied back on a second stream so the D2H of chunk c overlaps
+// the draw of chunk c+1.
+void draw_to_host(const wrs_sampler& s, uint64_t seed, uint64_t count, unsigned workers,
+                  uint32_t* out) {
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 26);
+    DevBuf b0(chunk * 4), b1(chunk * 4);
+    uint32_t* bufs[2] = {static_cast<uint32_t*>(b0.p), static_cast<uint32_t*>(b1.p)};
+    Stream copy;
+    cudaEvent_t drawn[2], copied[2];
+    for (int i = 0; i < 2; ++i) {
+        ck(cudaEventCreateWithFlags(&drawn[i], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(copied[i], copy.s), "event");
+    }
+    struct EvGuard {
+        cudaEvent_t* a;
+        cudaEvent_t* b;
+        ~EvGuard() {
+            for (int i = 0; i < 2; ++i) {
+                cudaEventDestroy(a[i]);
+                cudaEventDestroy(b[i]);
+            }
+        }
+    } eg{drawn, copied};
+    int c = 0;
+    for (uint64_t q = 0; q < count; q += chunk, c ^= 1) {
+        const uint64_t e = std::min(count, q + chunk);
+        ck(cudaStreamWaitEvent(s.stream->s, copied[c], 0), "wait");
+        ck(wrsb::launch_sample(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, q, e, count,
+                               workers, 0, bufs[c], s.stream->s),
+           "K5 launch");
+        ck(cudaEventRecord(drawn[c], s.stream->s), "event");
+        ck(cudaStreamWaitEvent(copy.s, drawn[c], 0), "wait");
+        ck(cudaMemcpyAsync(out + q, bufs[c], (e - q) * 4, cudaMemcpyDeviceToHost, copy.s), "D2H");
+        ck(cudaEventRecord(copied[c], copy.s), "event");
+    }
+    ck(cudaStreamSynchronize(copy.s), "draw");
+    ck(cudaStreamSynchronize(s.stream->s), "draw");
+}
+
+// implied_masses (verify.hpp:43-54): Kahan per item in bucket order, so the
+// result is the reference's bit for bit.  Verification utility, not the hot
+// path; runs over a D2H copy of the table.
+double max_rel_mass_error(const wrs_sampler& s) {
+    std::vector<Bucket> b(s.n);
+    ck(cudaMemcpy(b.data(), s.d_b(), s.n * sizeof(Bucket), cudaMemcpyDeviceToHost), "table D2H");
+    std::vector<double> sum(s.n, 0.0), comp(s.n, 0.0);
+    auto kadd = [&](uint32_t i, double x) {
+        const double y = x - comp[i];
+        const double t = sum[i] + y;
+        comp[i] = (t - sum[i]) - y;
+        sum[i] = t;
+    };
+    for (uint64_t i = 0; i < s.n; ++i) {
+        kadd(b[i].item, b[i].share);
+        kadd(b[i].alias, s.wn - b[i].share);
+    }
+    const double* w = s.weights->host_values();
+    double worst = 0.0;
+    for (uint64_t i = 0; i < s.n; ++i) worst = std::max(worst, std::abs(sum[i] - w[i]) / w[i]);
+    return worst;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+const char* wrs_last_error(void) { return t_last_error.c_str(); }
+
+const char* wrs_status_name(wrs_status status) {
+    switch (status) {
+        case WRS_OK: return "WRS_OK";
+        case WRS_EINVAL: return "WRS_EINVAL";
+        case WRS_EIO: return "WRS_EIO";
+        case WRS_EFORMAT: return "WRS_EFORMAT";
+        case WRS_EVERIFY: return "WRS_EVERIFY";
+        case WRS_ENOMEM: return "WRS_ENOMEM";
+        case WRS_EINTERNAL: return "WRS_EINTERNAL";
+    }
+    return "WRS_UNKNOWN";
+}
+
+// ---- weights ---------------------------------------------------------------------
+wrs_status wrs_weights_from_array(const double* w, uint64_t n, wrs_weights** out) {
+    if (!w || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        *out = new wrs_weights{weights_from_host(w, n)};
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_weights_generate(const char* dist, double param, uint64_t n, uint64_t seed,
+                                wrs_weights** out) {
+    if (!dist || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        const std::string d = dist;
+        if (d == "uniform") {
+            auto wd = std::make_shared<WeightsData>();
+            wd->device = current_device();
+            wd->n = n;
+            if (n == 0) throw std::invalid_argument("weights: need at least one item");
+            wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
+            wd->d_w = static_cast<double*>(wd->storage->p);
+            Stream st;
+            ck(wrsb::launch_generate_uniform(wd->d_w, n, 0, seed, st.s), "generate");
+            ck(cudaStreamSynchronize(st.s), "generate");
+            finalize_weights(*wd, "");
+            *out = new wrs_weights{wd};
+            return WRS_OK;
+        }
+        if (d == "powerlaw") {
+            const auto w = powerlaw_host(n, param, seed);
+            *out = new wrs_weights{weights_from_host(w.data(), n)};
+            return WRS_OK;
+        }
+        return fail(WRS_EINVAL, "unknown distribution: " + d);
+    });
+}
+
+// WRS1 file: "WRS1", u64 count, f64[count] (weight_file.hpp:57-101).
+wrs_status wrs_weights_read(const char* path, wrs_weights** out) {
+    if (!path || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        const std::string p = path;
+        std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path, "rb"), &std::fclose);
+        if (!f) throw io_error("cannot open for reading: " + p);
+        char magic[4];
+        uint64_t count = 0;
+        if (std::fread(magic, 1, 4, f.get()) != 4) throw format_error("truncated header: " + p);
+        if (std::memcmp(magic, "WRS1", 4) != 0)
+            throw format_error("bad magic, not a weight file: " + p);
+        if (std::fread(&count, sizeof count, 1, f.get()) != 1)
+            throw format_error("truncated count: " + p);
+        if (count > (uint64_t{1} << 40)) throw format_error("implausible item count: " + p);
+        std::vector<double> w(count);
+        if (count > 0 && std::fread(w.data(), sizeof(double), count, f.get()) != count)
+            throw format_error("truncated payload: " + p);
+        *out = new wrs_weights{weights_from_host(w.data(), count, p)};
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_weights_write(const wrs_weights* w, const char* path) {
+    if (!w || !path) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        const std::string p = path;
+        const double* v = w->data->host_values();
+        const uint64_t count = w->data->n;
+        std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path, "wb"), &std::fclose);
+        if (!f) throw io_error("cannot open for writing: " + p);
+        if (std::fwrite("WRS1", 1, 4, f.get()) != 4 ||
+            std::fwrite(&count, sizeof count, 1, f.get()) != 1 ||
+            (count > 0 && std::fwrite(v, sizeof(double), count, f.get()) != count))
+            throw io_error("short write: " + p);
+        if (std::fflush(f.get()) != 0) throw io_error("flush failed: " + p);
+        return WRS_OK;
+    });
+}
+
+uint64_t wrs_weights_count(const wrs_weights* w) { return w ? w->data->n : 0; }
+
+const double* wrs_weights_values(const wrs_weights* w) {
+    if (!w) return nullptr;
+    try {
+        return w->data->host_values();
+    } catch (const std::exception& e) {
+        fail(WRS_EINTERNAL, e.what());
+        return nullptr;
+    }
+}
+
+void wrs_weights_free(wrs_weights* w) { delete w; }
+
+// ---- sampler ---------------------------------------------------------------------
+wrs_status wrs_sampler_build(const wrs_weights* w, const char* algo, unsigned workers,
+                             uint64_t groups, wrs_sampler** out) {
+    (void)groups;
+    if (!w || !algo || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        const std::string name = algo;
+        uint64_t P;
+        if (name == "psa")
+            P = wrsb::default_jobs(w->data->n);
+        else if (name == "psa-exact")
+            P = std::max(1u, workers);
+        else if (name == "vose" || name == "sweep" || name == "2lvl-classic" ||
+                 name == "2lvl-sweep" || name == "compressed")
+            return fail(WRS_EINVAL, "sampler algorithm " + name +
+                                        " is not part of the B200 PSA path (use \"psa\")");
+        else
+            return fail(WRS_EINVAL, "unknown sampler algorithm: " + name);
+        *out = build_psa(w->data, P, 0, name.c_str()).release();
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_sampler_verify_masses(const wrs_sampler* s, double rel_tol) {
+    if (!s) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        const double worst = max_rel_mass_error(*s);
+        if (worst > rel_tol)
+            return fail(WRS_EVERIFY, "mass deviation " + std::to_string(worst) +
+                                         " exceeds tolerance in " + s->algo);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_sampler_draw(const wrs_sampler* s, uint64_t seed, uint64_t count,
+                            unsigned workers, uint32_t* out) {
+    if (!s || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        workers = workers ? workers : 1;
+        if (count == 0) return WRS_OK;
+        if (is_device_pointer(out)) {
+            ck(wrsb::launch_sample(s->d_b(), s->n, s->wn, seed, wrsb::kSampleStream, 0, count,
+                                   count, workers, 0, out, s->stream->s),
+               "K5 launch");
+            ck(cudaStreamSynchronize(s->stream->s), "draw");
+        } else {
+            draw_to_host(*s, seed, count, workers, out);
+        }
+        return WRS_OK;
+    });
+}
+
+void wrs_sampler_free(wrs_sampler* s) { delete s; }
+
+// ---- outside the hot path --------------------------------------------------------
+static wrs_status not_in_path(const char* what) {
+    return fail(WRS_EINVAL, std::string(what) + " is not part of the B200 PSA path");
+}
+
+wrs_status wrs_sample_with_replacement(const wrs_weights*, uint64_t, uint64_t, unsigned,
+                                       uint32_t*, uint64_t*, uint64_t*) {
+    return not_in_path("wrs_sample_with_replacement");
+}
+wrs_status wrs_sample_without_replacement(const wrs_weights*, uint64_t, uint64_t, unsigned,
+                                          uint32_t*) {
+    return not_in_path("wrs_sample_without_replacement");
+}
+wrs_status wrs_permutation(const wrs_weights*, uint64_t, unsigned, uint32_t*) {
+    return not_in_path("wrs_permutation");
+}
+wrs_status wrs_subset_sample(const wrs_weights*, uint64_t, unsigned, uint32_t*, uint64_t*) {
+    return not_in_path("wrs_subset_sample");
+}
+wrs_status wrs_reservoir_create(uint64_t, unsigned, uint64_t, wrs_reservoir** out) {
+    if (out) *out = nullptr;
+    return not_in_path("wrs_reservoir_create");
+}
+wrs_status wrs_reservoir_push(wrs_reservoir*, const uint32_t*, const double*, uint64_t) {
+    return not_in_path("wrs_reservoir_push");
+}
+wrs_status wrs_reservoir_items(const wrs_reservoir*, uint32_t*, double*, uint64_t*) {
+    return not_in_path("wrs_reservoir_items");
+}
+double wrs_reservoir_threshold(const wrs_reservoir*) {
+    return std::numeric_limits<double>::quiet_NaN();
+}
+void wrs_reservoir_free(wrs_reservoir*) {}
+wrs_status wrs_verify(const char*, uint64_t, int) { return not_in_path("wrs_verify"); }
+
+// ---- B200 extensions -------------------------------------------------------------
+uint64_t wrs_b200_default_jobs(uint64_t n) { return wrsb::default_jobs(n); }
+
+wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
+                                        wrs_weights** out) {
+    if (!d_w || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        auto wd = std::make_shared<WeightsData>();
+        wd->device = current_device();
+        wd->n = n;
+        if (n == 0) throw std::invalid_argument("weights: need at least one item");
+        if (copy) {
+            wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
+            wd->d_w = static_cast<double*>(wd->storage->p);
+            ck(cudaMemcpy(wd->d_w, d_w, n * sizeof(double), cudaMemcpyDeviceToDevice), "D2D");
+        } else {
+            wd->d_w = const_cast<double*>(d_w);
+            wd->owned = false;
+        }
+        finalize_weights(*wd, "");
+        *out = new wrs_weights{wd};
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_weights_generate_range(const char* dist, double param, uint64_t n_total,
+                                           uint64_t lo, uint64_t hi, uint64_t seed,
+                                           wrs_weights** out) {
+    (void)param;
+    if (!dist || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        if (std::string(dist) != "uniform")
+            return fail(WRS_EINVAL, "only \"uniform\" is generated per range on the device");
+        if (lo >= hi || hi > n_total) return fail(WRS_EINVAL, "bad range");
+        auto wd = std::make_shared<WeightsData>();
+        wd->device = current_device();
+        wd->n = hi - lo;
+        wd->storage = std::make_unique<DevBuf>(wd->n * sizeof(double));
+        wd->d_w = static_cast<double*>(wd->storage->p);
+        Stream st;
+        ck(wrsb::launch_generate_uniform(wd->d_w, wd->n, lo, seed, st.s), "generate");
+        ck(cudaStreamSynchronize(st.s), "generate");
+        finalize_weights(*wd, "");
+        *out = new wrs_weights{wd};
+        return WRS_OK;
+    });
+}
+
+double wrs_b200_weights_total(const wrs_weights* w) {
+    return w ? w->data->total : std::numeric_limits<double>::quiet_NaN();
+}
+const double* wrs_b200_weights_device(const wrs_weights* w) { return w ? w->data->d_w : nullptr; }
+
+wrs_status wrs_b200_sampler_build_psa(const wrs_weights* w, uint64_t jobs, unsigned flags,
+                                      wrs_sampler** out) {
+    if (!w || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        const uint64_t P = jobs ? jobs : wrsb::default_jobs(w->data->n);
+        if (P > std::numeric_limits<unsigned>::max())
+            throw std::invalid_argument("job count limited to 2^32-1");
+        *out = build_psa(w->data, P, flags, jobs ? "psa-exact" : "psa").release();
+        return WRS_OK;
+    });
+}
+
+uint64_t wrs_b200_sampler_jobs(const wrs_sampler* s) { return s ? s->P : 0; }
+uint64_t wrs_b200_sampler_size(const wrs_sampler* s) { return s ? s->n : 0; }
+double wrs_b200_sampler_bucket_mean(const wrs_sampler* s) {
+    return s ? s->wn : std::numeric_limits<double>::quiet_NaN();
+}
+double wrs_b200_sampler_total(const wrs_sampler* s) {
+    return s ? s->total : std::numeric_limits<double>::quiet_NaN();
+}
+const void* wrs_b200_sampler_device_buckets(const wrs_sampler* s) {
+    return s ? static_cast<const void*>(s->d_b()) : nullptr;
+}
+
+wrs_status wrs_b200_sampler_copy_buckets(const wrs_sampler* s, void* host_out) {
+    if (!s || !host_out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(s->stream->s), "sync");
+        ck(cudaMemcpy(host_out, s->d_b(), s->n * sizeof(Bucket), cudaMemcpyDeviceToHost), "D2H");
+        return WRS_OK;
+    });
+}
+
+int wrs_b200_set_timing(int on) { return g_timing.exchange(on ? 1 : 0); }
+
+wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream) {
+    if (!s) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(s->mu);
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        if (!s->ws.sc) ck(wrsb::workspace_alloc(s->ws, s->n, s->P), "workspace");
+        s->keep_ws = true;
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        s->timed = g_timing.load() != 0;
+        if (s->timed && !s->ev[0])
+            for (cudaEvent_t& e : s->ev) ck(cudaEventCreate(&e), "event");
+        ck(wrsb::launch_psa_build(s->weights->d_w, s->n, s->P, s->d_b(), s->ws, st,
+                                  s->timed ? s->ev : nullptr),
+           "PSA launch");
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_check(const wrs_sampler* s) {
+    if (!s) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        if (s->ws.sc) read_scalars(const_cast<wrs_sampler&>(*s));
+        return WRS_OK;
+    });
+}
+
+int wrs_b200_sampler_stage_times(const wrs_sampler* s, float* ms, int max) {
+    if (!s || !ms || !s->timed || !s->ev[0]) return 0;
+    int w = 0;
+    for (int i = 0; i < 7 && w < max; ++i) {
+        if (cudaEventElapsedTime(&ms[w], s->ev[i], s->ev[i + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            return w;
+        }
+        ++w;
+    }
+    return w;
+}
+
+wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t seed, uint64_t count,
+                                        unsigned workers, uint32_t* d_out, void* stream) {
+    if (!s || (!d_out && count)) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        ck(wrsb::launch_sample(s->d_b(), s->n, s->wn, seed, wrsb::kSampleStream, 0, count, count,
+                               workers ? workers : 1, 0, d_out, st),
+           "K5 launch");
+        return WRS_OK;
+    });
+}
+
+// Shard g draws AliasTable(shard_g).sample_many(seed_g, count, 1) with
+// seed_g = RngStream(seed, 'sdrw').derive(g).key, then adds the shard base.
+uint64_t wrs_b200_shard_seed(uint64_t seed, uint64_t shard) {
+    return wrsb::rng_derive(wrsb::rng_key(seed, 0x73647277u), shard);
+}
+
+wrs_status wrs_b200_sampler_draw_shard_device(const wrs_sampler* s, uint64_t seed, uint64_t shard,
+                                              uint64_t count, uint64_t base, uint32_t* d_out,
+                                              void* stream) {
+    if (!s || (!d_out && count)) return fail(WRS_EINVAL, "null argument");
+    if (base + s->n > (uint64_t{1} << 32)) return fail(WRS_EINVAL, "global ids exceed 2^32");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        ck(wrsb::launch_sample(s->d_b(), s->n, s->wn, wrs_b200_shard_seed(seed, shard),
+                               wrsb::kSampleStream, 0, count, count, 1,
+                               static_cast<uint32_t>(base), d_out, st),
+           "K5 launch");
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name, void* host_out,
+                                  uint64_t capacity, uint64_t* bytes) {
+    if (!s || !name || !bytes) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        if (!s->ws.sc) return fail(WRS_EINVAL, "build without WRS_B200_KEEP_WORKSPACE");
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        wrsb::DevScalars sc{};
+        ck(cudaMemcpy(&sc, s->ws.sc, sizeof sc, cudaMemcpyDeviceToHost), "D2H");
+        const uint64_t nl = sc.nl, nh = sc.nh;
+        const uint64_t nbl = (nl + 2047) / 2048, nbh = (nh + 2047) / 2048;
+        const std::string nm = name;
+        const void* src = nullptr;
+        uint64_t by = 0;
+        uint64_t counts[2] = {nl, nh};
+        if (nm == "counts") {
+            src = counts;
+            by = sizeof counts;
+        } else if (nm == "light") {
+            src = s->ws.lidx;
+            by = nl * 4;
+        } else if (nm == "heavy") {
+            src = s->ws.hidx;
+            by = nh * 4;
+        } else if (nm == "light_w") {
+            src = s->ws.lw;
+            by = nl * 8;
+        } else if (nm == "heavy_w") {
+            src = s->ws.hw;
+            by = nh * 8;
+        } else if (nm == "light_prefix") {
+            src = s->ws.lpre;
+            by = (nl + 1) * 8;
+        } else if (nm == "heavy_prefix") {
+            src = s->ws.hpre;
+            by = (nh + 1) * 8;
+        } else if (nm == "block_totals") {
+            src = s->ws.totals;
+            by = (nbl + nbh) * 8;
+        } else if (nm == "carries") {
+            src = s->ws.carries;
+            by = (nbl + nbh) * 8;
+        } else if (nm == "split_light") {
+            src = s->ws.split_l;
+            by = (s->P + 1) * 4;
+        } else if (nm == "split_heavy") {
+            src = s->ws.split_h;
+            by = (s->P + 1) * 4;
+        } else if (nm == "split_spill") {
+            src = s->ws.split_s;
+            by = (s->P + 1) * 8;
+        } else {
+            return fail(WRS_EINVAL, "unknown stage: " + nm);
+        }
+        *bytes = by;
+        if (!host_out) return WRS_OK;
+        if (capacity < by) return fail(WRS_EINVAL, "stage buffer too small");
+        if (nm == "counts")
+            std::memcpy(host_out, counts, by);
+        else if (by)
+            ck(cudaMemcpy(host_out, src, by, cudaMemcpyDeviceToHost), "D2H");
+        return WRS_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// paper_1903_00227_b200/csrc/common.cuh -- device-side building blocks shared
+// by the PSA build (psa_kernels.cu) and the query kernel (sample_kernels.cu).
+//
+// Everything here reproduces a reference primitive bit for bit; the whole
+// library is compiled with --fmad=false so no multiply-add is ever contracted
+// (the reference's x86-64 build has no FMA).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wrsb {
+
+// 16-byte bucket with the byte layout of wrs::alias_bucket (alias.hpp:26-33):
+// share at offset 0, item at 8, alias at 12.  Every bucket's item is its own
+// index, so a query reads one aligned 16-B record = one 32-B sector.
+struct alignas(16) Bucket {
+    double share;
+    uint32_t item;
+    uint32_t alias;
+};
+static_assert(sizeof(Bucket) == 16, "bucket must stay 16 bytes");
+
+// Device-resident scalars of one build (no host round trip between kernels).
+struct DevScalars {
+    double total;                  // pairwise W (weights.hpp:19-28)
+    double wn;                     // W / n (alias.hpp:247-248)
+    unsigned long long bad_index;  // first non-finite / non-positive weight, ~0 if none
+    unsigned long long nl, nh;     // light / heavy counts (alias.hpp:41-46)
+    unsigned int tile_counter;     // K1 dynamic tile ids
+    unsigned int plan_error;       // psa_plan's logic_error (alias.hpp:230-231)
+};
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;  // rng.hpp:23
+
+// SplitMix64 finalizer, rng.hpp:16-20.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// RngStream(seed, stream).key (rng.hpp:36-37) and derive(salt).key (:40-45).
+__host__ __device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t stream) {
+    return mix64(mix64(seed + kGolden) ^ mix64(stream) ^ stream);
+}
+__host__ __device__ __forceinline__ uint64_t rng_derive(uint64_t key, uint64_t salt) {
+    return mix64(key + mix64(salt + kGolden));
+}
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+#if defined(__CUDACC__)
+// Neumaier compensated sum, parallel.hpp:70-81 (the isfinite guard keeps an
+// infinite running value from poisoning the low word).
+struct CompSum {
+    double hi, lo;
+    __device__ __forceinline__ void add(double x) {
+        const double t = hi + x;
+        if (isfinite(t)) lo += fabs(hi) >= fabs(x) ? (hi - t) + x : (x - t) + hi;
+        hi = t;
+    }
+    __device__ __forceinline__ double value() const { return hi + lo; }
+};
+
+// std::min / std::max argument order (the reference's share clamps).
+__device__ __forceinline__ double std_min(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
+
+// ---- async copies (sm_80+ LDGSTS; no register staging) --------------------
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// 16-byte streaming store of one bucket.
+__device__ __forceinline__ void store_bucket(Bucket* b, uint64_t idx, double share,
+                                             uint32_t item, uint32_t alias) {
+    const unsigned long long s = static_cast<unsigned long long>(__double_as_longlong(share));
+    uint4 v = make_uint4(static_cast<unsigned>(s), static_cast<unsigned>(s >> 32), item, alias);
+    *reinterpret_cast<uint4*>(b + idx) = v;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace wrsb

@@ -1,0 +1,74 @@
+// paper_1903_00227_b200/csrc/engine.h -- host-side interface between the C ABI
+// (capi.cpp) and the kernels (psa_kernels.cu, sample_kernels.cu).  Internal:
+// not installed, not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace wrsb {
+
+// PSA job count used by algo "psa": one job = one thread's sequential pack
+// chain, so P sets the build's parallelism.  Fixed per n (DESIGN.md "Job
+// count") so tables are reproducible on any GPU and launch shape.
+constexpr uint64_t kJobBuckets = 1024;
+inline uint64_t default_jobs(uint64_t n) {
+    const uint64_t p = (n + kJobBuckets - 1) / kJobBuckets;
+    return p ? p : 1;
+}
+
+// Scratch of one build, sized for n items and P jobs.  Light and heavy lists
+// each get n slots (their split is only known on the device).
+struct Workspace {
+    uint64_t n = 0, P = 0;
+    int k0_depth = 0;
+    double* node_val = nullptr;      // K0 pairwise tree nodes above the CTA cut
+    unsigned* node_cnt = nullptr;    // K0 arrival counters
+    unsigned long long* tile_status = nullptr;  // K1 decoupled look-back
+    uint32_t* lidx = nullptr;        // light item ids, ascending
+    uint32_t* hidx = nullptr;        // heavy item ids, ascending
+    double* lw = nullptr;            // gathered light weights
+    double* hw = nullptr;            // gathered heavy weights
+    double* lpre = nullptr;          // exclusive light prefix, nl + 1 entries
+    double* hpre = nullptr;          // exclusive heavy prefix, nh + 1 entries
+    double* totals = nullptr;        // K2a block totals (light blocks, then heavy)
+    double* carries = nullptr;       // K2b exclusive carries
+    uint32_t* split_l = nullptr;     // K3 boundaries, P + 1
+    uint32_t* split_h = nullptr;
+    double* split_s = nullptr;       // spill entering each job
+    DevScalars* sc = nullptr;
+    uint64_t bytes = 0;
+};
+
+cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P);
+// Only what K0 needs (weights handles: validation + total).
+cudaError_t workspace_alloc_total(Workspace& ws, uint64_t n);
+void workspace_free(Workspace& ws);
+
+// K0: validation + bit-exact pairwise total of d_w into ws.sc (total, wn,
+// bad_index).  Asynchronous.
+cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStream_t st);
+
+// K0..K4: full PSA build into d_b.  `ev` (8 events or null) brackets the
+// stages for timing.  Asynchronous; errors are latched in ws.sc.
+cudaError_t launch_psa_build(const double* d_w, uint64_t n, uint64_t P, Bucket* d_b,
+                             Workspace& ws, cudaStream_t st, cudaEvent_t* ev);
+
+// K5: AliasTable::sample_many(seed, k, workers) (alias.hpp:274-284), output
+// positions [q_begin, q_end) of the k into d_out[0 .. q_end - q_begin).
+// `stream_id` is the reference's sample stream 0x616c6961 ("alia").  `base` is
+// added to every output (global ids of a shard).
+constexpr uint64_t kSampleStream = 0x616c6961u;
+cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
+                          uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
+                          uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st);
+
+// generate_uniform on the device (weight_file.hpp:32-38): counter-based, so
+// every element is independent and bit-exact; items [offset, offset + n) of
+// the global vector (a shard's slice).
+cudaError_t launch_generate_uniform(double* d_w, uint64_t n, uint64_t offset, uint64_t seed,
+                                    cudaStream_t st);
+
+}  // namespace wrsb

@@ -1,0 +1,822 @@
+// paper_1903_00227_b200/csrc/psa_kernels.cu -- the PSA alias-table build on
+// sm_100a.  Five stages, each bit-exact with the reference CPU code it
+// replaces (line citations are to /root/reference/proj):
+//
+//   K0  k_total        WeightTable ctor: validation + pairwise_sum tree
+//                      (weights.hpp:19-46), one CTA per subtree, top of the
+//                      tree combined by arrival counters.
+//   K1  k_partition    partition_items' stable light/heavy split
+//                      (alias.hpp:48-80): one pass, decoupled look-back,
+//                      emits ids AND gathered weights.
+//   K2a k_scan_blocks  prefix_sums pass 1 (parallel.hpp:110-115): Neumaier
+//                      total of every 2048-element block, thread per block,
+//                      warp-transposed through shared memory.
+//   K2b k_scan_carry   pass 2 (:116-121): serial Neumaier chain of the block
+//                      totals, light and heavy lists in parallel.
+//   K2c k_scan_blocks  pass 3 (:122-129): block chains seeded with the carry,
+//                      writing the exclusive prefix arrays (alias.hpp:82-95).
+//   K3  k_split        psa_split binary searches (alias.hpp:122-149), the
+//                      same probe sequence, one thread per split.
+//   K4  k_pack         psa_pack (alias.hpp:160-209), one lane per job, run in
+//                      S-step phases over per-lane windows staged by warp-wide
+//                      coalesced async copies; buckets flushed per phase.
+//
+// No stage needs a host round trip: counts live in DevScalars and every grid
+// is sized from upper bounds.
+#include <cstdio>
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "engine.h"
+
+namespace wrsb {
+
+// ===========================================================================
+// K0: validation + pairwise total
+// ===========================================================================
+constexpr int K0_NODE = 4096;   // max items of one CTA's subtree
+constexpr int K0_THREADS = 128; // >= leaves per subtree (4096 / 32)
+
+__device__ __forceinline__ int pad32(int e) { return e + (e >> 5); }
+
+// (start, size) of node t at `depth` of the floor-halving tree over [0, n)
+// (weights.hpp:26-27: left half = n/2).  Caller guarantees every node above
+// `depth` is internal.
+__host__ __device__ __forceinline__ void tree_node(uint64_t n, int depth, uint64_t t,
+                                                   uint64_t& start, uint64_t& size) {
+    start = 0;
+    size = n;
+    for (int l = 0; l < depth; ++l) {
+        const uint64_t half = size / 2;
+        if ((t >> (depth - 1 - l)) & 1) {
+            start += half;
+            size -= half;
+        } else {
+            size = half;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(K0_THREADS)
+k_total(const double* __restrict__ w, uint64_t n, int D, double* node_val,
+        unsigned* node_cnt, DevScalars* sc) {
+    __shared__ double buf[K0_NODE + K0_NODE / 32];
+    __shared__ double val[K0_THREADS];
+    const int tid = threadIdx.x;
+    const uint64_t t = blockIdx.x;
+    uint64_t s0, m64;
+    tree_node(n, D, t, s0, m64);
+    const int m = static_cast<int>(m64);
+
+    // coalesced load + validation (weights.hpp:36-41)
+    unsigned long long bad = ~0ull;
+    for (int base = 0; base < m; base += K0_THREADS * 8) {
+        double xs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * K0_THREADS + tid;
+            xs[u] = e < m ? __ldg(w + s0 + e) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * K0_THREADS + tid;
+            if (e < m) {
+                const double x = xs[u];
+                if (!isfinite(x) || !(x > 0.0)) bad = min(bad, static_cast<unsigned long long>(s0 + e));
+                buf[pad32(e)] = x;
+            }
+        }
+    }
+    if (bad != ~0ull) atomicMin(&sc->bad_index, bad);
+
+    // subtree depth: smallest d with ceil(m / 2^d) <= 32
+    int ds = 0;
+    while (((m64 + (1ull << ds) - 1) >> ds) > 32) ++ds;
+    __syncthreads();
+
+    // leaves: sequential sums of <= 32 items (weights.hpp:20-24)
+    if (tid < (1 << ds)) {
+        uint64_t s = 0, sz = m64;
+        bool rep = true;
+        for (int l = 0; l < ds; ++l) {
+            if (sz <= 32) {
+                rep = (tid & ((1 << (ds - l)) - 1)) == 0;
+                break;
+            }
+            const uint64_t half = sz / 2;
+            if ((tid >> (ds - 1 - l)) & 1) {
+                s += half;
+                sz -= half;
+            } else {
+                sz = half;
+            }
+        }
+        if (rep) {
+            double acc = 0.0;
+            for (int i = 0; i < static_cast<int>(sz); ++i) acc += buf[pad32(static_cast<int>(s) + i)];
+            val[tid] = acc;
+        }
+    }
+    // internal nodes inside the subtree: left + right (weights.hpp:27)
+    for (int l = ds - 1; l >= 0; --l) {
+        __syncthreads();
+        if (tid < (1 << l)) {
+            uint64_t sz = m64;
+            bool exists = true;
+            for (int i = 0; i < l; ++i) {
+                if (sz <= 32) {
+                    exists = false;
+                    break;
+                }
+                sz = ((tid >> (l - 1 - i)) & 1) ? sz - sz / 2 : sz / 2;
+            }
+            if (exists && sz > 32) {
+                const int slot = tid << (ds - l);
+                val[slot] = val[slot] + val[slot + (1 << (ds - l - 1))];
+            }
+        }
+    }
+    __syncthreads();
+    if (tid != 0) return;
+
+    // climb the tree above the cut: the second child to arrive adds.
+    double v = val[0];
+    uint64_t u = t;
+    int l = D;
+    node_val[((1ull << l) - 1) + u] = v;
+    while (l > 0) {
+        __threadfence();
+        const unsigned old = atomicAdd(&node_cnt[((1ull << (l - 1)) - 1) + (u >> 1)], 1u);
+        if (old == 0) return;
+        __threadfence();
+        const uint64_t left = u & ~1ull;
+        const double vl = __ldcg(&node_val[((1ull << l) - 1) + left]);
+        const double vr = __ldcg(&node_val[((1ull << l) - 1) + left + 1]);
+        v = vl + vr;
+        --l;
+        u >>= 1;
+        node_val[((1ull << l) - 1) + u] = v;
+    }
+    sc->total = v;
+    sc->wn = v / static_cast<double>(n);  // alias.hpp:50
+}
+
+// ===========================================================================
+// K1: stable light/heavy partition with decoupled look-back
+// ===========================================================================
+constexpr int K1_THREADS = 256;
+constexpr int K1_ROWS = 16;
+constexpr int K1_TILE = K1_THREADS * K1_ROWS;  // 4096
+constexpr int K1_SLOTS = K1_ROWS * (K1_THREADS / 32);  // 128 (row, warp) cells
+constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62,
+                             VAL_MASK = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
+    *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+__global__ void __launch_bounds__(K1_THREADS)
+k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
+            unsigned long long* status, uint32_t* __restrict__ lidx, double* __restrict__ lw,
+            uint32_t* __restrict__ hidx, double* __restrict__ hw) {
+    extern __shared__ __align__(16) unsigned char k1_smem[];
+    double* sw = reinterpret_cast<double*>(k1_smem);                     // K1_TILE
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(sw + K1_TILE);          // K1_TILE
+    uint32_t* cntL = sidx + K1_TILE;                                     // K1_SLOTS
+    uint32_t* cntH = cntL + K1_SLOTS;                                    // K1_SLOTS
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_excl;
+    __shared__ uint32_t s_totL, s_totH;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(&sc->tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * K1_TILE;
+    const double wn = __ldcg(&sc->wn);
+
+    double xs[K1_ROWS];
+    unsigned lm[K1_ROWS], hm[K1_ROWS];
+#pragma unroll
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const uint64_t gi = base + r * K1_THREADS + tid;
+        xs[r] = gi < n ? __ldg(w + gi) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const uint64_t gi = base + r * K1_THREADS + tid;
+        const bool valid = gi < n;
+        const bool light = valid && xs[r] <= wn;  // ties are light (alias.hpp:60)
+        lm[r] = __ballot_sync(0xffffffffu, light);
+        hm[r] = __ballot_sync(0xffffffffu, valid && !light);
+        if (lane == 0) {
+            cntL[r * 8 + warp] = __popc(lm[r]);
+            cntH[r * 8 + warp] = __popc(hm[r]);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // exclusive scans over the 128 (row, warp) cells in index order
+        uint32_t a[4], b[4], sa = 0, sb = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            a[q] = cntL[lane * 4 + q];
+            b[q] = cntH[lane * 4 + q];
+            sa += a[q];
+            sb += b[q];
+        }
+        uint32_t ia = sa, ib = sb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o);
+            const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o);
+            if (lane >= o) {
+                ia += ya;
+                ib += yb;
+            }
+        }
+        uint32_t ea = ia - sa, eb = ib - sb;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            cntL[lane * 4 + q] = ea;
+            cntH[lane * 4 + q] = eb;
+            ea += a[q];
+            eb += b[q];
+        }
+        const uint32_t totL = __shfl_sync(0xffffffffu, ia, 31);
+        const uint32_t totH = __shfl_sync(0xffffffffu, ib, 31);
+
+        // decoupled look-back for the number of lights before this tile
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile(&status[0], FLAG_P | totL);
+        } else {
+            if (lane == 0) st_volatile(&status[tile], FLAG_A | totL);
+            long long p = static_cast<long long>(tile) - 1;
+            while (true) {
+                const long long idx = p - lane;
+                unsigned long long v = FLAG_P;
+                if (idx >= 0) {
+                    do {
+                        v = ld_volatile(&status[idx]);
+                    } while ((v >> 62) == 0);
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                unsigned long long c = v & VAL_MASK;
+                if (pm) {
+                    const int first = __ffs(pm) - 1;
+                    if (lane > first) c = 0;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                excl += c;
+                if (pm) break;
+                p -= 32;
+            }
+            if (lane == 0) st_volatile(&status[tile], FLAG_P | (excl + totL));
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            s_totL = totL;
+            s_totH = totH;
+            if (tile + 1 == ntiles) {
+                sc->nl = excl + totL;
+                sc->nh = n - (excl + totL);
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t totL = s_totL, totH = s_totH;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const uint64_t gi = base + r * K1_THREADS + tid;
+        if ((lm[r] >> lane) & 1) {
+            const uint32_t p = cntL[r * 8 + warp] + __popc(lm[r] & lt);
+            sidx[p] = static_cast<uint32_t>(gi);
+            sw[p] = xs[r];
+        } else if ((hm[r] >> lane) & 1) {
+            const uint32_t p = totL + cntH[r * 8 + warp] + __popc(hm[r] & lt);
+            sidx[p] = static_cast<uint32_t>(gi);
+            sw[p] = xs[r];
+        }
+    }
+    __syncthreads();
+    const uint64_t L0 = s_excl, H0 = base - s_excl;
+    for (uint32_t p = tid; p < totL; p += K1_THREADS) {
+        lidx[L0 + p] = sidx[p];
+        lw[L0 + p] = sw[p];
+    }
+    for (uint32_t p = tid; p < totH; p += K1_THREADS) {
+        hidx[H0 + p] = sidx[totL + p];
+        hw[H0 + p] = sw[totL + p];
+    }
+}
+
+// ===========================================================================
+// K2a / K2c: per-2048-block Neumaier chains, one lane per block
+// ===========================================================================
+constexpr int SCAN_BLOCK = 2048;  // kScanBlock, parallel.hpp:60
+constexpr int K2_WARPS = 2;
+constexpr int K2_C = 32;          // chunk of each block staged per step
+
+struct K2Lane {
+    const double* src;
+    double* dst;
+    int len;
+};
+
+// PASS3 = false: pass 1 (block totals).  PASS3 = true: pass 3 (prefixes).
+template <bool PASS3>
+__global__ void __launch_bounds__(K2_WARPS * 32)
+k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
+              double* __restrict__ lpre, double* __restrict__ hpre, const DevScalars* sc,
+              double* __restrict__ totals, const double* __restrict__ carries) {
+    __shared__ double tile[K2_WARPS][2][32][K2_C + 1];
+    __shared__ K2Lane lanes[K2_WARPS][32];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t b = (static_cast<uint64_t>(blockIdx.x) * K2_WARPS + wq) * 32 + lane;
+
+    K2Lane me{nullptr, nullptr, 0};
+    if (b < nbl) {
+        me.src = lw + b * SCAN_BLOCK;
+        me.dst = lpre + 1 + b * SCAN_BLOCK;
+        me.len = static_cast<int>(umin64(SCAN_BLOCK, nl - b * SCAN_BLOCK));
+    } else if (b - nbl < nbh) {
+        const uint64_t hb = b - nbl;
+        me.src = hw + hb * SCAN_BLOCK;
+        me.dst = hpre + 1 + hb * SCAN_BLOCK;
+        me.len = static_cast<int>(umin64(SCAN_BLOCK, nh - hb * SCAN_BLOCK));
+    }
+    lanes[wq][lane] = me;
+    int maxlen = me.len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    if (maxlen == 0) return;
+    __syncwarp();
+
+    const int nchunks = (maxlen + K2_C - 1) / K2_C;
+    auto load_chunk = [&](int c, int buf) {
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            const K2Lane L = lanes[wq][r];
+            const int e = c * K2_C + lane;
+            if (e < L.len) cp_async8(&tile[wq][buf][r][lane], L.src + e);
+        }
+        cp_async_commit();
+    };
+
+    CompSum cs{0.0, 0.0};
+    if (PASS3 && me.len > 0) cs.add(carries[b]);  // run.add(carry[b]), parallel.hpp:124
+    load_chunk(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) {
+            load_chunk(c + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const int cnt = min(K2_C, me.len - c * K2_C);
+        double* row = tile[wq][buf][lane];
+        for (int e = 0; e < cnt; ++e) {
+            cs.add(row[e]);
+            if (PASS3) row[e] = cs.value();  // out[i] = run.value(), :127
+        }
+        __syncwarp();
+        if (PASS3) {
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r) {
+                const K2Lane L = lanes[wq][r];
+                const int e = c * K2_C + lane;
+                if (e < L.len) L.dst[e] = tile[wq][buf][r][lane];
+            }
+            __syncwarp();
+        }
+    }
+    if (!PASS3 && me.len > 0) totals[b] = cs.value();  // carry[b] = local.value(), :114
+}
+
+// ===========================================================================
+// K2b: serial carry chain over the block totals (parallel.hpp:116-121)
+// ===========================================================================
+constexpr int K2B_CHUNK = 1024;
+
+__global__ void __launch_bounds__(32)
+k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* carries,
+             double* lpre, double* hpre) {
+    __shared__ double buf[2][K2B_CHUNK];
+    const int lane = threadIdx.x;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const bool heavy = blockIdx.x == 1;
+    const uint64_t nb = heavy ? nbh : nbl;
+    const uint64_t off = heavy ? nbl : 0;
+    if (lane == 0) (heavy ? hpre : lpre)[0] = 0.0;  // prefix[0] = 0, alias.hpp:89
+    if (nb == 0) return;
+    const double* src = totals + off;
+    double* dst = carries + off;
+    const uint64_t nchunks = (nb + K2B_CHUNK - 1) / K2B_CHUNK;
+    auto load = [&](uint64_t c, int bsel) {
+        for (int i = lane; i < K2B_CHUNK; i += 32) {
+            const uint64_t g = c * K2B_CHUNK + i;
+            if (g < nb) cp_async8(&buf[bsel][i], src + g);
+        }
+        cp_async_commit();
+    };
+    CompSum acc{0.0, 0.0};
+    load(0, 0);
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const int bsel = static_cast<int>(c & 1);
+        if (c + 1 < nchunks) {
+            load(c + 1, bsel ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int cnt = static_cast<int>(umin64(K2B_CHUNK, nb - c * K2B_CHUNK));
+            for (int i = 0; i < cnt; ++i) {
+                const double t = buf[bsel][i];
+                dst[c * K2B_CHUNK + i] = acc.value();
+                acc.add(t);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// K3: split points (psa_split, alias.hpp:122-149) -- one thread per split
+// ===========================================================================
+__global__ void __launch_bounds__(256)
+k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__ lpre,
+        const double* __restrict__ hpre, const double* __restrict__ hw, uint32_t* split_l,
+        uint32_t* split_h, double* split_s) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    if (nh == 0) return;  // uniform fill, K4
+    const double wn = sc->wn;
+    if (k == 0) {
+        split_l[0] = 0;
+        split_h[0] = 0;
+        split_s[0] = hw[0];  // carry of job 0 = w(heavy[0]), alias.hpp:219
+        split_l[P] = static_cast<uint32_t>(nl);
+        split_h[P] = static_cast<uint32_t>(nh);
+        split_s[P] = 0.0;
+    }
+    if (k + 1 >= P) return;
+    const uint64_t m = n * (k + 1);
+    const uint64_t np = m / P + (m % P != 0);  // alias.hpp:227
+    const double target = static_cast<double>(np) * wn;
+    uint64_t lo = np > nl ? np - nl : 0;
+    uint64_t hi = np < nh ? np : nh;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        double f;
+        if (mid >= nh)
+            f = CUDART_INF;
+        else
+            f = (__ldg(lpre + (np - mid)) + __ldg(hpre + mid)) + __ldg(hw + mid);
+        if (f > target)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    double spill = 0.0;
+    if (lo < nh) {
+        const double x = (__ldg(hw + lo) + (__ldg(lpre + (np - lo)) + __ldg(hpre + lo))) - target;
+        spill = std_max(0.0, x);
+    }
+    split_l[k + 1] = static_cast<uint32_t>(np - lo);
+    split_h[k + 1] = static_cast<uint32_t>(lo);
+    split_s[k + 1] = spill;
+}
+
+// ===========================================================================
+// K4: pack (psa_pack, alias.hpp:160-209) -- one lane per job
+// ===========================================================================
+constexpr int K4_S = 32;      // steps per phase (= max items consumed per list)
+constexpr int K4_WARPS = 2;
+constexpr int K4_LW = K4_S + 1;   // light window row stride
+constexpr int K4_HW = K4_S + 2;   // heavy window row stride (S + 1 lookahead)
+
+enum : int { ST_MAIN = 0, ST_TAILA = 1, ST_TAILB = 2, ST_DONE = 3 };
+
+struct K4Smem {
+    double lw[32][K4_LW];
+    uint32_t lix[32][K4_LW];
+    uint32_t lal[32][K4_LW];
+    double hw[32][K4_HW];
+    uint32_t hix[32][K4_HW];
+    uint32_t hal[32][K4_HW];
+};
+
+__global__ void __launch_bounds__(K4_WARPS * 32)
+k_pack(uint64_t n, uint64_t P, const double* __restrict__ w, DevScalars* sc,
+       const uint32_t* __restrict__ lidx, const double* __restrict__ lw,
+       const uint32_t* __restrict__ hidx, const double* __restrict__ hw,
+       const uint32_t* __restrict__ split_l, const uint32_t* __restrict__ split_h,
+       const double* __restrict__ split_s, Bucket* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char k4_smem[];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    K4Smem& S = reinterpret_cast<K4Smem*>(k4_smem)[wq];
+    const uint64_t nh = sc->nh;
+    const double wn = sc->wn;
+
+    if (nh == 0) {
+        // fill_uniform_if_no_heavy (alias.hpp:288-297): every bucket keeps its item
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+             i += stride)
+            store_bucket(out, i, w[i], static_cast<uint32_t>(i), static_cast<uint32_t>(i));
+        return;
+    }
+
+    const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * K4_WARPS + wq) * 32 + lane;
+    uint64_t i = 0, lhi = 0, j = 0, hhi = 0;
+    int state = ST_DONE;
+    CompSum rem{0.0, 0.0};
+    if (k < P) {
+        i = split_l[k];
+        lhi = split_l[k + 1];
+        j = split_h[k];
+        hhi = split_h[k + 1];
+        if (lhi < i || hhi < j) {
+            atomicOr(&sc->plan_error, 1u);  // alias.hpp:230-231
+        } else {
+            state = ST_MAIN;
+            rem.hi = j < nh ? split_s[k] : CUDART_INF;  // alias.hpp:168
+        }
+    }
+
+    while (__any_sync(0xffffffffu, state != ST_DONE)) {
+        // ---- windows for this phase --------------------------------------
+        const bool live = state != ST_DONE;
+        const uint64_t wl0 = i;
+        const int lcnt = live ? static_cast<int>(umin64(K4_S, lhi - i)) : 0;
+        const uint64_t wh0 = min(j, nh - 1);
+        const uint64_t hend = min(min(j + K4_S + 1, hhi + 1), nh);
+        const int hcnt = live ? static_cast<int>(hend - wh0) : 0;
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            const uint64_t rl0 = __shfl_sync(0xffffffffu, wl0, r);
+            const int rlc = __shfl_sync(0xffffffffu, lcnt, r);
+            const uint64_t rh0 = __shfl_sync(0xffffffffu, wh0, r);
+            const int rhc = __shfl_sync(0xffffffffu, hcnt, r);
+            if (lane < rlc) {
+                cp_async8(&S.lw[r][lane], lw + rl0 + lane);
+                cp_async4(&S.lix[r][lane], lidx + rl0 + lane);
+            }
+            if (lane < rhc) {
+                cp_async8(&S.hw[r][lane], hw + rh0 + lane);
+                cp_async4(&S.hix[r][lane], hidx + rh0 + lane);
+            }
+            if (lane + 32 < rhc) {
+                cp_async8(&S.hw[r][lane + 32], hw + rh0 + lane + 32);
+                cp_async4(&S.hix[r][lane + 32], hidx + rh0 + lane + 32);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+
+        // ---- S sequential steps per lane ----------------------------------
+        const uint64_t i0 = i, j0 = j;
+        double cLw = S.lw[lane][0];
+        uint32_t cLix = S.lix[lane][0];
+        uint32_t hCur = S.hix[lane][0];  // heavy_at(j): slot of min(j, nh-1) = wh0
+        int qn = static_cast<int>(min(j + 1, nh - 1) - wh0);
+        uint32_t hNext = S.hix[lane][qn];
+        double hNextW = S.hw[lane][qn];
+        for (int step = 0; step < K4_S; ++step) {
+            if (state == ST_DONE) break;
+            const double v = rem.value();
+            if (state == ST_MAIN) {
+                if (v > wn) {
+                    if (i >= lhi) state = ST_TAILA;
+                } else {
+                    if (j >= hhi) state = ST_TAILB;
+                }
+            }
+            bool lightOp, addL = false;
+            if (state == ST_MAIN) {
+                lightOp = v > wn;
+                addL = lightOp;
+            } else if (state == ST_TAILA) {
+                if (j >= hhi) {
+                    state = ST_DONE;
+                    break;
+                }
+                lightOp = false;
+            } else {  // ST_TAILB
+                if (i >= lhi) {
+                    state = ST_DONE;
+                    break;
+                }
+                lightOp = true;
+            }
+            if (lightOp) {
+                // buckets[idx] = {w, {idx, heavy_at(j)}} (alias.hpp:186-189, 194-197)
+                const int p = static_cast<int>(i - wl0);
+                S.lal[lane][p] = hCur;
+                if (addL) rem.add(cLw - wn);
+                ++i;
+                const int pn = min(p + 1, K4_S - 1);
+                cLw = S.lw[lane][pn];
+                cLix = S.lix[lane][pn];
+            } else {
+                // buckets[idx] = {clamp(rem), {idx, heavy_at(j+1)}} (alias.hpp:175-183, 200-206)
+                const int p = static_cast<int>(j - wh0);
+                const double share = state == ST_MAIN ? std_max(0.0, std_min(v, wn)) : std_min(v, wn);
+                S.hw[lane][p] = share;
+                S.hal[lane][p] = hNext;
+                if (j + 1 < nh) {
+                    rem.add(hNextW - wn);
+                } else {
+                    rem.hi = state == ST_MAIN ? CUDART_INF : wn;
+                    rem.lo = 0.0;
+                }
+                ++j;
+                hCur = hNext;
+                qn = min(static_cast<int>(min(j + 1, nh - 1) - wh0), K4_HW - 1);
+                hNext = S.hix[lane][qn];
+                hNextW = S.hw[lane][qn];
+            }
+        }
+        (void)cLix;
+        __syncwarp();
+
+        // ---- flush this phase's buckets ------------------------------------
+        const int nlw = static_cast<int>(i - i0);
+        const int nhw = static_cast<int>(j - j0);
+        const int hoff = static_cast<int>(j0 - wh0);
+#pragma unroll 2
+        for (int r = 0; r < 32; ++r) {
+            const int rl = __shfl_sync(0xffffffffu, nlw, r);
+            const int rh = __shfl_sync(0xffffffffu, nhw, r);
+            const int ro = __shfl_sync(0xffffffffu, hoff, r);
+            if (lane < rl) {
+                const uint32_t idx = S.lix[r][lane];
+                store_bucket(out, idx, S.lw[r][lane], idx, S.lal[r][lane]);
+            }
+            if (lane < rh) {
+                const uint32_t idx = S.hix[r][ro + lane];
+                store_bucket(out, idx, S.hw[r][ro + lane], idx, S.hal[r][ro + lane]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+static int k0_depth(uint64_t n) {
+    int D = 0;
+    while (((n + (1ull << D) - 1) >> D) > static_cast<uint64_t>(K0_NODE)) ++D;
+    return D;
+}
+
+cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P) {
+    workspace_free(ws);
+    ws.n = n;
+    ws.P = P;
+    ws.k0_depth = k0_depth(n);
+    const uint64_t nodes = (2ull << ws.k0_depth) - 1;
+    const uint64_t cnts = (1ull << ws.k0_depth);
+    const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
+    const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 2;
+    cudaError_t e;
+#define WS_ALLOC(ptr, count)                                                         \
+    do {                                                                             \
+        const uint64_t by_ = static_cast<uint64_t>(count) * sizeof(*(ptr)) + 64;     \
+        e = cudaMalloc(reinterpret_cast<void**>(&(ptr)), by_);                       \
+        if (e != cudaSuccess) {                                                      \
+            workspace_free(ws);                                                      \
+            return e;                                                                \
+        }                                                                            \
+        ws.bytes += by_;                                                             \
+    } while (0)
+    WS_ALLOC(ws.node_val, nodes);
+    WS_ALLOC(ws.node_cnt, cnts);
+    WS_ALLOC(ws.tile_status, ntiles);
+    WS_ALLOC(ws.lidx, n);
+    WS_ALLOC(ws.hidx, n);
+    WS_ALLOC(ws.lw, n);
+    WS_ALLOC(ws.hw, n);
+    WS_ALLOC(ws.lpre, n + 1);
+    WS_ALLOC(ws.hpre, n + 1);
+    WS_ALLOC(ws.totals, nblocks);
+    WS_ALLOC(ws.carries, nblocks);
+    WS_ALLOC(ws.split_l, P + 1);
+    WS_ALLOC(ws.split_h, P + 1);
+    WS_ALLOC(ws.split_s, P + 1);
+    WS_ALLOC(ws.sc, 1);
+#undef WS_ALLOC
+    return cudaSuccess;
+}
+
+cudaError_t workspace_alloc_total(Workspace& ws, uint64_t n) {
+    workspace_free(ws);
+    ws.n = n;
+    ws.k0_depth = k0_depth(n);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ws.node_val),
+                               ((2ull << ws.k0_depth) - 1) * sizeof(double));
+    if (e == cudaSuccess)
+        e = cudaMalloc(reinterpret_cast<void**>(&ws.node_cnt), (1ull << ws.k0_depth) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&ws.sc), sizeof(DevScalars));
+    if (e != cudaSuccess) workspace_free(ws);
+    return e;
+}
+
+void workspace_free(Workspace& ws) {
+    void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.lidx,    ws.hidx,
+                    ws.lw,       ws.hw,       ws.lpre,        ws.hpre,    ws.totals,
+                    ws.carries,  ws.split_l,  ws.split_h,     ws.split_s, ws.sc};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    ws = Workspace{};
+}
+
+static cudaError_t reset_scalars(Workspace& ws, cudaStream_t st) {
+    DevScalars init{};
+    init.bad_index = ~0ull;
+    // DevScalars is tiny: one async H2D from a constant pinned pattern is
+    // cheaper than several memsets, and the source outlives every copy.
+    static DevScalars* pinned = [&] {
+        DevScalars* p = nullptr;
+        if (cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(DevScalars)) != cudaSuccess)
+            return static_cast<DevScalars*>(nullptr);
+        *p = init;
+        return p;
+    }();
+    if (!pinned) return cudaErrorMemoryAllocation;
+    return cudaMemcpyAsync(ws.sc, pinned, sizeof(DevScalars), cudaMemcpyHostToDevice, st);
+}
+
+cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStream_t st) {
+    cudaError_t e = reset_scalars(ws, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ws.node_cnt, 0, sizeof(unsigned) << ws.k0_depth, st);
+    if (e != cudaSuccess) return e;
+    k_total<<<static_cast<unsigned>(1ull << ws.k0_depth), K0_THREADS, 0, st>>>(
+        d_w, n, ws.k0_depth, ws.node_val, ws.node_cnt, ws.sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_psa_build(const double* d_w, uint64_t n, uint64_t P, Bucket* d_b,
+                             Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
+    const int k1_smem = K1_TILE * 12 + 2 * K1_SLOTS * 4;
+    const int k4_smem = K4_WARPS * static_cast<int>(sizeof(K4Smem));
+    // per-device attribute; cheap enough to set on every build
+    cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
+    cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
+    const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
+    const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
+    const unsigned k2_grid = static_cast<unsigned>((nblocks + K2_WARPS * 32 - 1) / (K2_WARPS * 32));
+    const unsigned k3_grid = static_cast<unsigned>((P + 255) / 256);
+    const unsigned k4_grid = static_cast<unsigned>((P + K4_WARPS * 32 - 1) / (K4_WARPS * 32));
+    cudaError_t e;
+#define REC(i)                                          \
+    do {                                                \
+        if (ev) cudaEventRecord(ev[i], st);             \
+    } while (0)
+    REC(0);
+    e = launch_total(d_w, n, ws, st);
+    if (e != cudaSuccess) return e;
+    REC(1);
+    e = cudaMemsetAsync(ws.tile_status, 0, ntiles * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    k_partition<<<static_cast<unsigned>(ntiles), K1_THREADS, k1_smem, st>>>(
+        d_w, n, ntiles, ws.sc, ws.tile_status, ws.lidx, ws.lw, ws.hidx, ws.hw);
+    REC(2);
+    k_scan_blocks<false><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc,
+                                                            ws.totals, ws.carries);
+    REC(3);
+    k_scan_carry<<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
+    REC(4);
+    k_scan_blocks<true><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc,
+                                                           ws.totals, ws.carries);
+    REC(5);
+    k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
+                                     ws.split_s);
+    REC(6);
+    k_pack<<<k4_grid, K4_WARPS * 32, k4_smem, st>>>(n, P, d_w, ws.sc, ws.lidx, ws.lw, ws.hidx,
+                                                    ws.hw, ws.split_l, ws.split_h, ws.split_s,
+                                                    d_b);
+    REC(7);
+#undef REC
+    return cudaGetLastError();
+}
+
+}  // namespace wrsb

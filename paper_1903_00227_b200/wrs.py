@@ -1,0 +1,333 @@
+"""ctypes binding of libwrs_b200.so -- the reference's C ABI (include/wrs.h)
+plus the B200 extensions (include/wrs_b200.h).
+
+The classes mirror the reference's handle model (capi.cpp: wrs_weights,
+wrs_sampler) so the tests read like the reference's own test_capi.cpp.  There
+is no Python or CPU compute here: every method is one ABI call into the CUDA
+library, and loading fails loudly when the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libwrs_b200.so")
+
+WRS_OK, WRS_EINVAL, WRS_EIO, WRS_EFORMAT, WRS_EVERIFY, WRS_ENOMEM, WRS_EINTERNAL = range(7)
+KEEP_WORKSPACE = 1
+
+BUCKET_DTYPE = np.dtype([("share", "<f8"), ("item", "<u4"), ("alias", "<u4")])
+
+u64, f64, u32, vp = C.c_uint64, C.c_double, C.c_uint32, C.c_void_p
+
+# every symbol include/wrs.h and include/wrs_b200.h declare, with ctypes types
+SIGNATURES = {
+    "wrs_last_error": (C.c_char_p, []),
+    "wrs_status_name": (C.c_char_p, [C.c_int]),
+    "wrs_weights_from_array": (C.c_int, [vp, u64, C.POINTER(vp)]),
+    "wrs_weights_generate": (C.c_int, [C.c_char_p, f64, u64, u64, C.POINTER(vp)]),
+    "wrs_weights_read": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "wrs_weights_write": (C.c_int, [vp, C.c_char_p]),
+    "wrs_weights_count": (u64, [vp]),
+    "wrs_weights_values": (vp, [vp]),
+    "wrs_weights_free": (None, [vp]),
+    "wrs_sampler_build": (C.c_int, [vp, C.c_char_p, C.c_uint, u64, C.POINTER(vp)]),
+    "wrs_sampler_verify_masses": (C.c_int, [vp, f64]),
+    "wrs_sampler_draw": (C.c_int, [vp, u64, u64, C.c_uint, vp]),
+    "wrs_sampler_free": (None, [vp]),
+    "wrs_sample_with_replacement": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, vp]),
+    "wrs_sample_without_replacement": (C.c_int, [vp, u64, u64, C.c_uint, vp]),
+    "wrs_permutation": (C.c_int, [vp, u64, C.c_uint, vp]),
+    "wrs_subset_sample": (C.c_int, [vp, u64, C.c_uint, vp, vp]),
+    "wrs_reservoir_create": (C.c_int, [u64, C.c_uint, u64, C.POINTER(vp)]),
+    "wrs_reservoir_push": (C.c_int, [vp, vp, vp, u64]),
+    "wrs_reservoir_items": (C.c_int, [vp, vp, vp, vp]),
+    "wrs_reservoir_threshold": (f64, [vp]),
+    "wrs_reservoir_free": (None, [vp]),
+    "wrs_verify": (C.c_int, [C.c_char_p, u64, C.c_int]),
+    "wrs_b200_default_jobs": (u64, [u64]),
+    "wrs_b200_weights_from_device": (C.c_int, [vp, u64, C.c_int, C.POINTER(vp)]),
+    "wrs_b200_weights_generate_range": (C.c_int, [C.c_char_p, f64, u64, u64, u64, u64,
+                                                  C.POINTER(vp)]),
+    "wrs_b200_weights_total": (f64, [vp]),
+    "wrs_b200_weights_device": (vp, [vp]),
+    "wrs_b200_sampler_build_psa": (C.c_int, [vp, u64, C.c_uint, C.POINTER(vp)]),
+    "wrs_b200_sampler_jobs": (u64, [vp]),
+    "wrs_b200_sampler_size": (u64, [vp]),
+    "wrs_b200_sampler_bucket_mean": (f64, [vp]),
+    "wrs_b200_sampler_total": (f64, [vp]),
+    "wrs_b200_sampler_device_buckets": (vp, [vp]),
+    "wrs_b200_sampler_copy_buckets": (C.c_int, [vp, vp]),
+    "wrs_b200_sampler_rebuild_async": (C.c_int, [vp, vp]),
+    "wrs_b200_sampler_check": (C.c_int, [vp]),
+    "wrs_b200_sampler_draw_device": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp]),
+    "wrs_b200_sampler_stage": (C.c_int, [vp, C.c_char_p, vp, u64, C.POINTER(u64)]),
+    "wrs_b200_set_timing": (C.c_int, [C.c_int]),
+    "wrs_b200_sampler_stage_times": (C.c_int, [vp, C.POINTER(C.c_float), C.c_int]),
+    "wrs_b200_shard_range": (None, [u64, u64, u64, C.POINTER(u64), C.POINTER(u64)]),
+    "wrs_b200_shard_counts": (C.c_int, [vp, u64, u64, u64, vp]),
+    "wrs_b200_shard_seed": (u64, [u64, u64]),
+    "wrs_b200_sampler_draw_shard_device": (C.c_int, [vp, u64, u64, u64, u64, vp, vp]),
+}
+
+_lib = None
+
+
+class WrsError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{status_name(status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+def lib() -> C.CDLL:
+    """Load libwrs_b200.so; raise if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} missing: build it with `make -C paper_1903_00227_b200/csrc` "
+                "or __graft_entry__.build(); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def status_name(status: int) -> str:
+    return lib().wrs_status_name(status).decode()
+
+
+def last_error() -> str:
+    return lib().wrs_last_error().decode()
+
+
+def _check(status: int) -> None:
+    if status != WRS_OK:
+        raise WrsError(status, last_error())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(vp)
+
+
+def _dev_ptr(t) -> int:
+    """Device pointer of a torch tensor (or an int)."""
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def default_jobs(n: int) -> int:
+    return lib().wrs_b200_default_jobs(n)
+
+
+class Weights:
+    """wrs_weights handle (reference capi.cpp:33-35 / WeightTable)."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def from_array(cls, w) -> "Weights":
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        h = vp()
+        _check(lib().wrs_weights_from_array(_ptr(w), w.size, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def generate(cls, dist: str, param: float, n: int, seed: int) -> "Weights":
+        h = vp()
+        _check(lib().wrs_weights_generate(dist.encode(), param, n, seed, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def generate_range(cls, dist: str, param: float, n_total: int, lo: int, hi: int,
+                       seed: int) -> "Weights":
+        """B200 extension: items [lo, hi) of generate(dist, param, n_total, seed)."""
+        h = vp()
+        _check(lib().wrs_b200_weights_generate_range(dist.encode(), param, n_total, lo, hi,
+                                                     seed, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def read(cls, path: str) -> "Weights":
+        h = vp()
+        _check(lib().wrs_weights_read(os.fsencode(path), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, tensor, copy: bool = True) -> "Weights":
+        """B200 extension: weights already in HBM (a float64 CUDA tensor)."""
+        h = vp()
+        _check(lib().wrs_b200_weights_from_device(_dev_ptr(tensor), tensor.numel(),
+                                                  1 if copy else 0, C.byref(h)))
+        obj = cls(h)
+        obj._keepalive = tensor
+        return obj
+
+    def write(self, path: str) -> None:
+        _check(lib().wrs_weights_write(self.h, os.fsencode(path)))
+
+    def count(self) -> int:
+        return lib().wrs_weights_count(self.h)
+
+    def values(self) -> np.ndarray:
+        p = lib().wrs_weights_values(self.h)
+        if not p:
+            raise WrsError(WRS_EINTERNAL, last_error())
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), (self.count(),)).copy()
+
+    def total(self) -> float:
+        return lib().wrs_b200_weights_total(self.h)
+
+    def device_ptr(self) -> int:
+        return lib().wrs_b200_weights_device(self.h)
+
+    def free(self) -> None:
+        if self.h:
+            lib().wrs_weights_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Sampler:
+    """wrs_sampler handle (reference capi.cpp:37-49, AliasTable)."""
+
+    def __init__(self, handle, weights: Weights):
+        self.h = handle
+        self.weights = weights
+
+    @classmethod
+    def build(cls, weights: Weights, algo: str = "psa", workers: int = 1, groups: int = 0):
+        h = vp()
+        _check(lib().wrs_sampler_build(weights.h, algo.encode(), workers, groups, C.byref(h)))
+        return cls(h, weights)
+
+    @classmethod
+    def build_psa(cls, weights: Weights, jobs: int = 0, keep_workspace: bool = False):
+        h = vp()
+        _check(lib().wrs_b200_sampler_build_psa(weights.h, jobs,
+                                                KEEP_WORKSPACE if keep_workspace else 0,
+                                                C.byref(h)))
+        return cls(h, weights)
+
+    # reference surface ----------------------------------------------------
+    def verify_masses(self, rel_tol: float) -> int:
+        return lib().wrs_sampler_verify_masses(self.h, rel_tol)
+
+    def draw(self, seed: int, count: int, workers: int = 1, out: np.ndarray | None = None):
+        if out is None:
+            out = np.empty(count, np.uint32)
+        _check(lib().wrs_sampler_draw(self.h, seed, count, workers, _ptr(out)))
+        return out
+
+    def draw_into(self, seed: int, count: int, workers: int, out_ptr: int) -> None:
+        """wrs_sampler_draw with a raw pointer (pinned host or device)."""
+        _check(lib().wrs_sampler_draw(self.h, seed, count, workers, out_ptr))
+
+    # B200 extensions -------------------------------------------------------
+    @property
+    def jobs(self) -> int:
+        return lib().wrs_b200_sampler_jobs(self.h)
+
+    @property
+    def size(self) -> int:
+        return lib().wrs_b200_sampler_size(self.h)
+
+    @property
+    def bucket_mean(self) -> float:
+        return lib().wrs_b200_sampler_bucket_mean(self.h)
+
+    @property
+    def total(self) -> float:
+        return lib().wrs_b200_sampler_total(self.h)
+
+    def buckets(self) -> np.ndarray:
+        out = np.empty(self.size, BUCKET_DTYPE)
+        _check(lib().wrs_b200_sampler_copy_buckets(self.h, _ptr(out)))
+        return out
+
+    def device_buckets(self) -> int:
+        return lib().wrs_b200_sampler_device_buckets(self.h)
+
+    def rebuild_async(self, stream=None) -> None:
+        _check(lib().wrs_b200_sampler_rebuild_async(self.h, _stream_ptr(stream)))
+
+    def check(self) -> None:
+        _check(lib().wrs_b200_sampler_check(self.h))
+
+    def draw_device(self, seed: int, count: int, workers: int, out, stream=None) -> None:
+        _check(lib().wrs_b200_sampler_draw_device(self.h, seed, count, workers,
+                                                  _dev_ptr(out), _stream_ptr(stream)))
+
+    def draw_shard_device(self, seed: int, shard: int, count: int, base: int, out,
+                          stream=None) -> None:
+        _check(lib().wrs_b200_sampler_draw_shard_device(self.h, seed, shard, count, base,
+                                                        _dev_ptr(out), _stream_ptr(stream)))
+
+    def stage(self, name: str) -> np.ndarray:
+        dtypes = {"counts": np.uint64, "light": np.uint32, "heavy": np.uint32,
+                  "light_w": np.float64, "heavy_w": np.float64, "light_prefix": np.float64,
+                  "heavy_prefix": np.float64, "block_totals": np.float64,
+                  "carries": np.float64, "split_light": np.uint32, "split_heavy": np.uint32,
+                  "split_spill": np.float64}
+        nbytes = u64()
+        _check(lib().wrs_b200_sampler_stage(self.h, name.encode(), None, 0, C.byref(nbytes)))
+        dt = np.dtype(dtypes[name])
+        out = np.empty(nbytes.value // dt.itemsize, dt)
+        _check(lib().wrs_b200_sampler_stage(self.h, name.encode(), _ptr(out), nbytes.value,
+                                            C.byref(nbytes)))
+        return out
+
+    def stage_times(self) -> list[float]:
+        buf = (C.c_float * 8)()
+        k = lib().wrs_b200_sampler_stage_times(self.h, buf, 8)
+        return [buf[i] for i in range(k)]
+
+    def free(self) -> None:
+        if self.h:
+            lib().wrs_sampler_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def set_timing(on: bool) -> None:
+    lib().wrs_b200_set_timing(1 if on else 0)
+
+
+def shard_range(n: int, groups: int, g: int) -> tuple[int, int]:
+    lo, hi = u64(), u64()
+    lib().wrs_b200_shard_range(n, groups, g, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+def shard_counts(totals, seed: int, k: int) -> np.ndarray:
+    t = np.ascontiguousarray(totals, np.float64)
+    out = np.empty(t.size, np.uint64)
+    _check(lib().wrs_b200_shard_counts(_ptr(t), t.size, seed, k, _ptr(out)))
+    return out
+
+
+def shard_seed(seed: int, shard: int) -> int:
+    return lib().wrs_b200_shard_seed(seed, shard)

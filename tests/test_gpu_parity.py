@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI of libwrs_b200.so) against
+the oracle and the reference's golden vectors.
+
+Bar: buckets bit-exact (share, item, alias), bucket mean
+bit-exact, every intermediate stage bit-exact, draws bit-exact -- all at the
+same job count P, which is what the reference's table depends on.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1903_00227_b200 as wrs
+from tests.stats_util import chi_square
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def P():
+    return oracle.port()
+
+
+def build(w, jobs=0, keep=False):
+    W = wrs.Weights.from_array(w)
+    return W, wrs.Sampler.build_psa(W, jobs, keep)
+
+
+def assert_same_table(S, w, jobs, P):
+    ob, own = P.psa_build(w, jobs)
+    gb = S.buckets()
+    assert S.bucket_mean == own
+    if gb.tobytes() != ob.tobytes():
+        bad = np.nonzero(gb.view(np.uint8).reshape(-1, 16).any(1) !=
+                         ob.view(np.uint8).reshape(-1, 16).any(1))[0]
+        diff = np.nonzero((gb["share"] != ob["share"]) | (gb["alias"] != ob["alias"]) |
+                          (gb["item"] != ob["item"]))[0]
+        raise AssertionError(f"n={w.size} P={jobs}: {diff.size} buckets differ, first "
+                             f"{diff[:5]} gpu={gb[diff[:3]]} oracle={ob[diff[:3]]} {bad[:3]}")
+
+
+# ---- golden vectors ------------------------------------------------------------
+
+def test_golden_small_tables():
+    z = np.load(os.path.join(GOLD, "psa_small.npz"))
+    names = sorted({k.split("/")[0] for k in z.files})
+    for name in names:
+        w = z[f"{name}/w"]
+        W = wrs.Weights.from_array(w)
+        assert W.total() == z[f"{name}/total"], name
+        for jobs in (1, 2, 3, 4, 8):
+            S = wrs.Sampler.build_psa(W, jobs)
+            assert S.bucket_mean == z[f"{name}/P{jobs}/bucket_mean"]
+            assert S.buckets().tobytes() == z[f"{name}/P{jobs}/buckets"].tobytes(), (name, jobs)
+
+
+def test_golden_draws_through_abi():
+    d = np.load(os.path.join(GOLD, "draws_small.npz"))
+    W = wrs.Weights.from_array(d["w"])
+    S = wrs.Sampler.build(W, "psa-exact", 4)
+    assert S.buckets().tobytes() == d["buckets"].tobytes()
+    for Wk in (1, 3, 4, 8):
+        assert np.array_equal(S.draw(99, 100001, Wk), d[f"seed99_W{Wk}"]), Wk
+    assert np.array_equal(S.draw(100, 100001, 4), d["seed100_W4"])
+
+
+def test_golden_medium_generators_and_tables():
+    m = np.load(os.path.join(GOLD, "psa_medium.npz"))
+    cases = {"uniform_1e6_s42": ("uniform", 0.0, 10**6, 42),
+             "powerlaw1_1e6_s42": ("powerlaw", 1.0, 10**6, 42),
+             "powerlaw05_2e5_s7": ("powerlaw", 0.5, 200_000, 7)}
+    for tag, (dist, s, n, seed) in cases.items():
+        W = wrs.Weights.generate(dist, s, n, seed)
+        assert sha(W.values()) == str(m[f"{tag}/w_sha"]), tag
+        assert W.total() == m[f"{tag}/total"]
+        jobs_keys = sorted({int(k.split("/")[1][1:]) for k in m.files if k.startswith(tag + "/P")})
+        assert wrs.default_jobs(n) in jobs_keys
+        for jobs in jobs_keys:
+            S = wrs.Sampler.build_psa(W, jobs)
+            assert sha(S.buckets()) == str(m[f"{tag}/P{jobs}/buckets_sha"]), (tag, jobs)
+        S = wrs.Sampler.build_psa(W, -(-n // 128))
+        for Wk in (1, 8):
+            s_ = S.draw(42, 10**6, Wk)
+            assert sha(s_) == str(m[f"{tag}/draw_P{-(-n // 128)}_seed42_k1e6_W{Wk}_sha"])
+
+
+# ---- per-stage parity ------------------------------------------------------------
+
+def test_stages_bit_exact(P):
+    rng = np.random.default_rng(11)
+    inputs = [P.generate_uniform(30011, 3), P.generate_powerlaw(20000, 1.0, 4),
+              np.concatenate([np.full(5000, 1.0), rng.random(5000) + 0.5])]
+    for w in inputs:
+        for jobs in (1, 13, wrs.default_jobs(w.size), 977):
+            W, S = build(w, jobs, keep=True)
+            part = P.partition(w)
+            nl, nh = S.stage("counts")
+            assert (nl, nh) == (part["light"].size, part["heavy"].size)
+            assert np.array_equal(S.stage("light"), part["light"])
+            assert np.array_equal(S.stage("heavy"), part["heavy"])
+            assert np.array_equal(S.stage("light_w"), w[part["light"]])
+            assert np.array_equal(S.stage("heavy_w"), w[part["heavy"]])
+            tot = np.concatenate([P.scan_block_totals(w[part["light"]]),
+                                  P.scan_block_totals(w[part["heavy"]])])
+            assert S.stage("block_totals").tobytes() == tot.tobytes()
+            nbl = (part["light"].size + 2047) // 2048
+            car = np.concatenate([P.scan_carries(tot[:nbl]), P.scan_carries(tot[nbl:])])
+            assert S.stage("carries").tobytes() == car.tobytes()
+            assert S.stage("light_prefix").tobytes() == part["light_prefix"].tobytes()
+            assert S.stage("heavy_prefix").tobytes() == part["heavy_prefix"].tobytes()
+            if nh:
+                bounds, spill = P.psa_plan(w, jobs)
+                sl, sh, ss = S.stage("split_light"), S.stage("split_heavy"), S.stage("split_spill")
+                assert np.array_equal(sl[1:], bounds[:, 1].astype(np.uint32))
+                assert np.array_equal(sh[1:], bounds[:, 3].astype(np.uint32))
+                assert ss[:-1].tobytes() == spill.tobytes()
+            assert_same_table(S, w, jobs, P)
+
+
+# ---- randomized table parity -------------------------------------------------------
+
+def weight_cases(P):
+    rng = np.random.default_rng(2024)
+    yield "one", np.array([7.0])
+    yield "two_tiny", np.array([1.0, 1e-12])
+    yield "equal", np.full(1000, 0.25)
+    yield "huge_heavy", np.concatenate([[1e6], np.ones(9999)])
+    for n in (2, 3, 31, 32, 33, 100, 2047, 2048, 2049, 4095, 4096, 4097, 8193, 65537, 250_000):
+        yield f"u{n}", P.generate_uniform(n, n + 1)
+        yield f"pl1_{n}", P.generate_powerlaw(n, 1.0, n + 2)
+    for n in (1000, 100_000):
+        yield f"pl2_{n}", P.generate_powerlaw(n, 2.0, 5)
+        yield f"pl05_{n}", P.generate_powerlaw(n, 0.5, 6)
+        yield f"logn_{n}", np.exp(rng.normal(0.0, 2.0, n))
+        t = np.ones(n)
+        t[:: 50] = 9.0
+        yield f"ties_{n}", t
+        x = rng.random(n) + 0.5
+        x[rng.random(n) < 0.5] = 1.0
+        yield f"mixties_{n}", x
+        yield f"skew_{n}", 10.0 ** rng.uniform(-12, 12, n)
+
+
+def test_random_tables_bit_exact(P):
+    for name, w in weight_cases(P):
+        W = wrs.Weights.from_array(w)
+        n = w.size
+        for jobs in sorted({1, 3, wrs.default_jobs(n), max(1, n // 7), n, 2 * n + 1}):
+            if jobs > 4 * 10**6:
+                continue
+            S = wrs.Sampler.build_psa(W, jobs)
+            assert S.jobs == jobs
+            assert_same_table(S, w, jobs, P)
+
+
+def test_default_psa_is_reference_at_default_jobs(P):
+    w = P.generate_uniform(300_000, 9)
+    W = wrs.Weights.from_array(w)
+    S = wrs.Sampler.build(W, "psa", 8)
+    assert S.jobs == wrs.default_jobs(w.size)
+    assert_same_table(S, w, S.jobs, P)
+    S2 = wrs.Sampler.build(W, "psa-exact", 8)
+    assert S2.jobs == 8
+    assert_same_table(S2, w, 8, P)
+
+
+# ---- draws ------------------------------------------------------------------------
+
+def test_draws_bit_exact_random(P):
+    import torch
+    for n, k, Wk in ((1, 1000, 1), (17, 12345, 3), (1000, 10**6, 8), (100_000, 3 * 10**6 + 7, 13),
+                     (4097, 5, 16)):
+        w = P.generate_powerlaw(n, 1.0, 3) if n > 1 else np.array([2.0])
+        W, S = build(w)
+        b = S.buckets()
+        ref = P.sample_many(b, S.bucket_mean, 77, k, Wk)
+        assert np.array_equal(S.draw(77, k, Wk), ref), (n, k, Wk)
+        out = torch.empty(k, dtype=torch.int32, device="cuda")
+        S.draw_device(77, k, Wk, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+
+
+def test_draw_zero_and_workers_zero(P):
+    W, S = build(P.generate_uniform(100, 1))
+    assert S.draw(5, 0, 1).size == 0
+    assert np.array_equal(S.draw(5, 1000, 0), S.draw(5, 1000, 1))  # capi.cpp:213
+
+
+# ---- reference test_capi.cpp behaviour ----------------------------------------------
+
+def test_capi_lifecycle_like_reference(tmp_path):  # test_capi.cpp:12-74
+    w = np.array([3.0, 1, 1, 1])
+    W = wrs.Weights.from_array(w)
+    assert W.count() == 4 and np.array_equal(W.values(), w)
+    with pytest.raises(wrs.WrsError) as e:
+        wrs.Weights.from_array(np.array([1.0, -1.0]))
+    assert e.value.status == 1 and "item 1" in e.value.message
+    gen = wrs.Weights.generate("powerlaw", 1.5, 500, 42)
+    path = str(tmp_path / "rt.wrs")
+    gen.write(path)
+    back = wrs.Weights.read(path)
+    assert np.array_equal(back.values(), gen.values())
+    with pytest.raises(wrs.WrsError) as e:
+        wrs.Weights.read(str(tmp_path / "missing.wrs"))
+    assert e.value.status == 2
+    (tmp_path / "garbage.bin").write_bytes(b"not a weight file at all")
+    with pytest.raises(wrs.WrsError) as e:
+        wrs.Weights.read(str(tmp_path / "garbage.bin"))
+    assert e.value.status == 3
+    with pytest.raises(wrs.WrsError):
+        wrs.Weights.generate("cauchy", 0, 10, 1)
+
+    pl = wrs.Weights.generate("powerlaw", 2.0, 1000, 7)
+    S = wrs.Sampler.build(pl, "psa", 4)
+    assert S.verify_masses(1e-9) == 0
+    out = S.draw(123, 10000, 2)
+    assert out.max() < 1000
+    assert np.array_equal(out, S.draw(123, 10000, 2))
+    with pytest.raises(wrs.WrsError):
+        wrs.Sampler.build(pl, "bogus", 1)
+
+
+def test_bad_weight_file_payload(tmp_path):
+    path = tmp_path / "bad.wrs"
+    vals = np.array([1.0, 2.0, np.nan, 4.0])
+    path.write_bytes(b"WRS1" + np.uint64(4).tobytes() + vals.tobytes())
+    with pytest.raises(wrs.WrsError) as e:
+        wrs.Weights.read(str(path))
+    assert e.value.status == 3 and "weight 2" in e.value.message
+
+
+# ---- full size (BASELINE config 2: n=1e8 uniform, k=1e9) ------------------------------
+
+def test_full_size_table_and_draws(P):
+    import torch
+    n, k = 10**8, 10**9
+    m = np.load(os.path.join(GOLD, "psa_medium.npz"))
+    W = wrs.Weights.generate("uniform", 0.0, n, 42)
+    w = W.values()
+    assert sha(w) == str(m["uniform_1e8_s42/w_sha"])
+    S = wrs.Sampler.build(W, "psa", 1)
+    jobs = S.jobs
+    # bytewise parity with the oracle at the same job count, full size
+    ob, own = P.psa_build(w, jobs)
+    gb = S.buckets()
+    assert own == S.bucket_mean
+    assert gb.tobytes() == ob.tobytes()
+    # the reference's own verification oracle (verify.hpp:43-98)
+    err = P.max_relative_mass_error(P.implied_masses(gb, own), w)
+    assert err < 1e-7
+    assert S.verify_masses(1e-7) == 0
+    # 1e9 draws: bitwise on sampled windows, chi-square on everything
+    out = torch.empty(k, dtype=torch.int32, device="cuda")
+    for Wk in (1, 148):
+        S.draw_device(2024, k, Wk, out)
+        torch.cuda.synchronize()
+        for lo in (0, 123_456_789, 499_999_000, k - 100_000):
+            ref = P.sample_range(gb, own, 2024, k, Wk, lo, lo + 100_000)
+            assert np.array_equal(out[lo:lo + 100_000].cpu().numpy().view(np.uint32), ref), (Wk, lo)
+    counts = torch.bincount(out.long(), minlength=n)
+    del out
+    wt = torch.from_numpy(w).cuda()
+    e = wt / wt.sum() * k
+    big = e >= 5.0
+    d = counts[big].double() - e[big]
+    stat = float((d * d / e[big]).sum())
+    cells = int(big.sum())
+    pe = float(e[~big].sum())
+    if pe > 0:
+        stat += (float(counts[~big].sum()) - pe) ** 2 / pe
+        cells += 1
+    from tests.stats_util import chi2_critical
+    crit = chi2_critical(cells - 1, 1e-3)
+    assert stat < crit, (stat, crit)
