@@ -256,6 +256,14 @@ def main():
         step()
     torch.cuda.synchronize()
     S.check()
+    # one extra untimed step with per-stage events (K0..K4) for the breakdown
+    wrs.set_timing(True)
+    step()
+    torch.cuda.synchronize()
+    stage_ms = S.stage_times()
+    wrs.set_timing(False)
+    step()  # re-arm the untimed path
+    torch.cuda.synchronize()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -305,7 +313,10 @@ def main():
         "build": {"gitems_per_s": n_local / (build_ms * 1e-3) / 1e9, "ms": build_ms,
                   "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": hbm,
                                "peak_kind": hbm_kind, "unit": "GB/s", "frac": build_gbs / hbm,
-                               "bytes_per_item": BUILD_BYTES_PER_ITEM}},
+                               "bytes_per_item": BUILD_BYTES_PER_ITEM},
+                  "stages_ms": dict(zip(["K0_total", "K1_partition", "K2a_block_totals",
+                                         "K2b_carries", "K2c_prefixes", "K3_splits", "K4_pack"],
+                                        [round(x, 4) for x in stage_ms]))},
         "sample": {"gsamples_per_s": k_per_rank / (draw_ms * 1e-3) / 1e9, "ms": draw_ms},
         "roofline": {"bound": "hbm", "kernel": "k_sample", "achieved": draw_gbs, "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s", "frac": draw_gbs / hbm,
