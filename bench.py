@@ -34,10 +34,11 @@ K_SAMPLES = 10**9
 SEED = 42
 METRIC = "alias build Gitems/s + sample Gsamples/s at 1/2/4/8 B200; % HBM roofline"
 UNIT = "G(items+samples)/s"
-BUILD_BYTES_PER_ITEM = 80   # K0 8 + K1 20 + K2 24 + K4 28
+BUILD_BYTES_PER_ITEM = 72   # SURVEY.md §8(d) minus K0 (W comes with the weights, as the
+                            # reference's WeightTable): K1 20 + K2 24 + K4 28
 SAMPLE_BYTES_PER_DRAW = 36  # one 32-B sector gather + one 4-B index store
-KERNELS_PER_STEP = 8        # k_total, k_partition, k_scan_blocks x2, k_scan_carry,
-                            # k_split, k_pack, k_sample
+KERNELS_PER_STEP = 8        # k_partition, k_scan_blocks x2, k_scan_carry, k_split,
+                            # k_pack, k_assemble, k_sample
 
 
 def parse():
@@ -314,8 +315,8 @@ def main():
                   "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": hbm,
                                "peak_kind": hbm_kind, "unit": "GB/s", "frac": build_gbs / hbm,
                                "bytes_per_item": BUILD_BYTES_PER_ITEM},
-                  "stages_ms": dict(zip(["K0_total", "K1_partition", "K2a_block_totals",
-                                         "K2b_carries", "K2c_prefixes", "K3_splits", "K4_pack"],
+                  "stages_ms": dict(zip(["K1_partition", "K2a_block_totals", "K2b_carries",
+                                         "K2c_prefixes", "K3_splits", "K4a_pack", "K4b_assemble"],
                                         [round(x, 4) for x in stage_ms]))},
         "sample": {"gsamples_per_s": k_per_rank / (draw_ms * 1e-3) / 1e9, "ms": draw_ms},
         "roofline": {"bound": "hbm", "kernel": "k_sample", "achieved": draw_gbs, "peak": hbm,

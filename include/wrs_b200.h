@@ -53,7 +53,8 @@ WRS_API double wrs_b200_sampler_total(const wrs_sampler* s);
 WRS_API const void* wrs_b200_sampler_device_buckets(const wrs_sampler* s);
 WRS_API wrs_status wrs_b200_sampler_copy_buckets(const wrs_sampler* s, void* host_out);
 
-/* Re-run the whole build (K0..K4) in place from the sampler's weights,
+/* Re-run the build (K1..K4b; W comes from the weights handle, as the
+ * reference's AliasTable takes it from its WeightTable) in place,
  * asynchronously on `stream`; no host synchronisation.  Plan errors are
  * latched on the device and reported by wrs_b200_sampler_check. */
 WRS_API wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream);
@@ -66,19 +67,20 @@ WRS_API wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t s
                                                 uint32_t* d_out, void* stream);
 
 /* Copy a named intermediate of the last build (needs WRS_B200_KEEP_WORKSPACE):
- * "counts" (u64 nl, nh), "light", "heavy" (u32), "light_w", "heavy_w" (f64),
+ * "counts" (u64 nl, nh), "heavy" (u32 heavy ids), "light_w", "heavy_w" (f64),
  * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries), "block_totals",
  * "carries" (f64, light blocks then heavy blocks), "split_light",
- * "split_heavy" (u32, P + 1), "split_spill" (f64, P + 1).  *bytes receives
- * the size; host_out may be NULL to query it. */
+ * "split_heavy" (u32, P + 1), "split_spill" (f64, P + 1), "light_alias"
+ * (u32, nl), "heavy_share" (f64, nh), "heavy_alias" (u32, nh).  *bytes
+ * receives the size; host_out may be NULL to query it. */
 WRS_API wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name,
                                           void* host_out, uint64_t capacity,
                                           uint64_t* bytes);
 
 /* Device time of each build stage of the last wrs_b200_sampler_rebuild_async
  * made with timing on (wrs_b200_set_timing(1)), in milliseconds:
- * [K0 total, K1 partition, K2a block totals, K2b carries, K2c prefixes,
- *  K3 splits, K4 pack].  Returns the number written. */
+ * [K1 partition, K2a block totals, K2b carries, K2c prefixes, K3 splits,
+ *  K4a pack, K4b assemble].  Returns the number written. */
 WRS_API int wrs_b200_set_timing(int on);
 WRS_API int wrs_b200_sampler_stage_times(const wrs_sampler* s, float* ms, int max);
 

@@ -205,10 +205,16 @@ struct wrs_sampler {
     cudaEvent_t ev[8] = {};
     bool timed = false;
     std::mutex mu;  // rebuild / stage access
+    // draw scratch (region plan), reused across draws; sws_ev orders users
+    mutable wrsb::SampleWorkspace sws;
+    mutable std::mutex sws_mu;
+    mutable cudaEvent_t sws_ev = nullptr;
 
     ~wrs_sampler() {
         if (device >= 0) cudaSetDevice(device);
         wrsb::workspace_free(ws);
+        if (sws_ev) cudaEventSynchronize(sws_ev), cudaEventDestroy(sws_ev);
+        sws.release();
         for (cudaEvent_t& e : ev)
             if (e) cudaEventDestroy(e);
     }
@@ -241,12 +247,27 @@ std::unique_ptr<wrs_sampler> build_psa(const std::shared_ptr<WeightsData>& wd, u
     s->keep_ws = flags & WRS_B200_KEEP_WORKSPACE;
     s->buckets = std::make_unique<DevBuf>(wd->n * sizeof(Bucket));
     s->stream = std::make_unique<Stream>();
-    ck(wrsb::workspace_alloc(s->ws, s->n, s->P), "workspace");
-    ck(wrsb::launch_psa_build(wd->d_w, s->n, s->P, s->d_b(), s->ws, s->stream->s, nullptr),
+    ck(wrsb::workspace_alloc(s->ws, s->n, s->P, s->keep_ws), "workspace");
+    ck(wrsb::launch_psa_build(wd->d_w, s->n, wd->total, s->P, s->d_b(), s->ws, s->stream->s,
+                              nullptr),
        "PSA launch");
     read_scalars(*s);
     if (!s->keep_ws) wrsb::workspace_free(s->ws);
     return s;
+}
+
+// One draw launch on stream st; the sampler's draw scratch is handed from
+// one draw to the next through sws_ev, so draws on different streams never
+// share it concurrently.
+void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, uint64_t k,
+               uint32_t workers, uint32_t base, uint32_t* out, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(s.sws_mu);
+    if (!s.sws_ev) ck(cudaEventCreateWithFlags(&s.sws_ev, cudaEventDisableTiming), "event");
+    ck(cudaStreamWaitEvent(st, s.sws_ev, 0), "wait");
+    ck(wrsb::launch_sample(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, q0, q1, k, workers, base,
+                           out, st, &s.sws),
+       "K5 launch");
+    ck(cudaEventRecord(s.sws_ev, st), "event");
 }
 
 bool is_device_pointer(const void* p) {
@@ -263,7 +284,7 @@ bool is_device_pointer(const void* p) {
 // the draw of chunk c+1.
 void draw_to_host(const wrs_sampler& s, uint64_t seed, uint64_t count, unsigned workers,
                   uint32_t* out) {
-    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 26);
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 28);
     DevBuf b0(chunk * 4), b1(chunk * 4);
     uint32_t* bufs[2] = {static_cast<uint32_t*>(b0.p), static_cast<uint32_t*>(b1.p)};
     Stream copy;
@@ -287,9 +308,7 @@ void draw_to_host(const wrs_sampler& s, uint64_t seed, uint64_t count, unsigned 
     for (uint64_t q = 0; q < count; q += chunk, c ^= 1) {
         const uint64_t e = std::min(count, q + chunk);
         ck(cudaStreamWaitEvent(s.stream->s, copied[c], 0), "wait");
-        ck(wrsb::launch_sample(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, q, e, count,
-                               workers, 0, bufs[c], s.stream->s),
-           "K5 launch");
+        sample_on(s, seed, q, e, count, workers, 0, bufs[c], s.stream->s);
         ck(cudaEventRecord(drawn[c], s.stream->s), "event");
         ck(cudaStreamWaitEvent(copy.s, drawn[c], 0), "wait");
         ck(cudaMemcpyAsync(out + q, bufs[c], (e - q) * 4, cudaMemcpyDeviceToHost, copy.s), "D2H");
@@ -476,9 +495,7 @@ wrs_status wrs_sampler_draw(const wrs_sampler* s, uint64_t seed, uint64_t count,
         workers = workers ? workers : 1;
         if (count == 0) return WRS_OK;
         if (is_device_pointer(out)) {
-            ck(wrsb::launch_sample(s->d_b(), s->n, s->wn, seed, wrsb::kSampleStream, 0, count,
-                                   count, workers, 0, out, s->stream->s),
-               "K5 launch");
+            sample_on(*s, seed, 0, count, count, workers, 0, out, s->stream->s);
             ck(cudaStreamSynchronize(s->stream->s), "draw");
         } else {
             draw_to_host(*s, seed, count, workers, out);
@@ -618,14 +635,13 @@ wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream) {
     return guarded([&] {
         std::lock_guard<std::mutex> g(s->mu);
         ck(cudaSetDevice(s->device), "cudaSetDevice");
-        if (!s->ws.sc) ck(wrsb::workspace_alloc(s->ws, s->n, s->P), "workspace");
-        s->keep_ws = true;
+        if (!s->ws.sc) ck(wrsb::workspace_alloc(s->ws, s->n, s->P, false), "workspace");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
         s->timed = g_timing.load() != 0;
         if (s->timed && !s->ev[0])
             for (cudaEvent_t& e : s->ev) ck(cudaEventCreate(&e), "event");
-        ck(wrsb::launch_psa_build(s->weights->d_w, s->n, s->P, s->d_b(), s->ws, st,
-                                  s->timed ? s->ev : nullptr),
+        ck(wrsb::launch_psa_build(s->weights->d_w, s->n, s->weights->total, s->P, s->d_b(),
+                                  s->ws, st, s->timed ? s->ev : nullptr),
            "PSA launch");
         return WRS_OK;
     });
@@ -660,9 +676,7 @@ wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t seed, uin
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
-        ck(wrsb::launch_sample(s->d_b(), s->n, s->wn, seed, wrsb::kSampleStream, 0, count, count,
-                               workers ? workers : 1, 0, d_out, st),
-           "K5 launch");
+        sample_on(*s, seed, 0, count, count, workers ? workers : 1, 0, d_out, st);
         return WRS_OK;
     });
 }
@@ -681,10 +695,8 @@ wrs_status wrs_b200_sampler_draw_shard_device(const wrs_sampler* s, uint64_t see
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
-        ck(wrsb::launch_sample(s->d_b(), s->n, s->wn, wrs_b200_shard_seed(seed, shard),
-                               wrsb::kSampleStream, 0, count, count, 1,
-                               static_cast<uint32_t>(base), d_out, st),
-           "K5 launch");
+        sample_on(*s, wrs_b200_shard_seed(seed, shard), 0, count, count, 1,
+                  static_cast<uint32_t>(base), d_out, st);
         return WRS_OK;
     });
 }
@@ -707,9 +719,15 @@ wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name, void* 
         if (nm == "counts") {
             src = counts;
             by = sizeof counts;
-        } else if (nm == "light") {
-            src = s->ws.lidx;
+        } else if (nm == "light_alias") {
+            src = s->ws.lalias;
             by = nl * 4;
+        } else if (nm == "heavy_share") {
+            src = s->ws.hshare;
+            by = nh * 8;
+        } else if (nm == "heavy_alias") {
+            src = s->ws.halias;
+            by = nh * 4;
         } else if (nm == "heavy") {
             src = s->ws.hidx;
             by = nh * 4;

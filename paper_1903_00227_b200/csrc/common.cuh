@@ -52,12 +52,18 @@ __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { re
 
 #if defined(__CUDACC__)
 // Neumaier compensated sum, parallel.hpp:70-81 (the isfinite guard keeps an
-// infinite running value from poisoning the low word).
+// infinite running value from poisoning the low word).  Written branch-free:
+// the error term is always computed and the guarded update is a select, so
+// the compiler can compute the error terms of a run of adds in parallel and
+// leave only one dependent DADD per add on each of the hi and lo chains.  The
+// values are identical to the guarded form.
 struct CompSum {
     double hi, lo;
     __device__ __forceinline__ void add(double x) {
         const double t = hi + x;
-        if (isfinite(t)) lo += fabs(hi) >= fabs(x) ? (hi - t) + x : (x - t) + hi;
+        const double e = fabs(hi) >= fabs(x) ? (hi - t) + x : (x - t) + hi;
+        const double l2 = lo + e;
+        lo = isfinite(t) ? l2 : lo;
         hi = t;
     }
     __device__ __forceinline__ double value() const { return hi + lo; }

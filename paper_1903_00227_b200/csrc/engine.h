@@ -27,12 +27,16 @@ struct Workspace {
     double* node_val = nullptr;      // K0 pairwise tree nodes above the CTA cut
     unsigned* node_cnt = nullptr;    // K0 arrival counters
     unsigned long long* tile_status = nullptr;  // K1 decoupled look-back
-    uint32_t* lidx = nullptr;        // light item ids, ascending
-    uint32_t* hidx = nullptr;        // heavy item ids, ascending
+    uint32_t* hidx = nullptr;        // heavy item ids, ascending (light ids stay implicit)
     double* lw = nullptr;            // gathered light weights
     double* hw = nullptr;            // gathered heavy weights
     double* lpre = nullptr;          // exclusive light prefix, nl + 1 entries
     double* hpre = nullptr;          // exclusive heavy prefix, nh + 1 entries
+    uint32_t* lalias = nullptr;      // K4a: alias of every light, list order
+    double* hshare = nullptr;        // K4a: share of every heavy, list order
+    uint32_t* halias = nullptr;      // K4a: alias of every heavy, list order
+    uint32_t* lalias_own = nullptr;  // separate storage (else lalias aliases lpre)
+    double* hshare_own = nullptr;    // separate storage (else hshare aliases hpre)
     double* totals = nullptr;        // K2a block totals (light blocks, then heavy)
     double* carries = nullptr;       // K2b exclusive carries
     uint32_t* split_l = nullptr;     // K3 boundaries, P + 1
@@ -42,7 +46,9 @@ struct Workspace {
     uint64_t bytes = 0;
 };
 
-cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P);
+// separate_outputs keeps K4a's outputs out of the prefix arrays' storage, so
+// every intermediate stays inspectable (WRS_B200_KEEP_WORKSPACE).
+cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate_outputs);
 // Only what K0 needs (weights handles: validation + total).
 cudaError_t workspace_alloc_total(Workspace& ws, uint64_t n);
 void workspace_free(Workspace& ws);
@@ -51,19 +57,33 @@ void workspace_free(Workspace& ws);
 // bad_index).  Asynchronous.
 cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStream_t st);
 
-// K0..K4: full PSA build into d_b.  `ev` (8 events or null) brackets the
-// stages for timing.  Asynchronous; errors are latched in ws.sc.
-cudaError_t launch_psa_build(const double* d_w, uint64_t n, uint64_t P, Bucket* d_b,
-                             Workspace& ws, cudaStream_t st, cudaEvent_t* ev);
+// K1..K4b: the PSA build of AliasTable(wt, psa, P) into d_b, given the
+// weights' pairwise total (computed once by K0 when the weights handle was
+// made, as WeightTable does).  `ev` (8 events or null) brackets the seven
+// stages for timing.  Asynchronous; plan errors are latched in ws.sc.
+cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
+                             Bucket* d_b, Workspace& ws, cudaStream_t st, cudaEvent_t* ev);
+
+// Scratch of the region-ordered draw plan (sample_kernels.cu); grows on demand.
+struct SampleWorkspace {
+    void* base = nullptr;
+    uint64_t bytes = 0;
+    unsigned* overflow = nullptr;  // device flag: a region slab overflowed (never expected)
+    cudaError_t reserve(uint64_t bytes);
+    void release();
+};
 
 // K5: AliasTable::sample_many(seed, k, workers) (alias.hpp:274-284), output
 // positions [q_begin, q_end) of the k into d_out[0 .. q_end - q_begin).
 // `stream_id` is the reference's sample stream 0x616c6961 ("alia").  `base` is
-// added to every output (global ids of a shard).
+// added to every output (global ids of a shard).  With a workspace, large
+// tables use the region-ordered plan; without, the direct gather kernel.
 constexpr uint64_t kSampleStream = 0x616c6961u;
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
-                          uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st);
+                          uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,
+                          SampleWorkspace* ws);
+bool use_region_plan(uint64_t n, uint64_t k);
 
 // generate_uniform on the device (weight_file.hpp:32-38): counter-based, so
 // every element is independent and bit-exact; items [offset, offset + n) of

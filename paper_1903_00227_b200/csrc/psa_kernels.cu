@@ -23,6 +23,7 @@
 //
 // No stage needs a host round trip: counts live in DevScalars and every grid
 // is sized from upper bounds.
+#include <atomic>
 #include <cstdio>
 #include <math_constants.h>
 
@@ -162,7 +163,10 @@ k_total(const double* __restrict__ w, uint64_t n, int D, double* node_val,
 }
 
 // ===========================================================================
-// K1: stable light/heavy partition with decoupled look-back
+// Tile classification shared by K1 (partition) and K4b (assemble): a tile of
+// K1_TILE items, row r covering items [r*256, r*256+256); per (row, warp)
+// ballots of light / heavy flags and exclusive light / heavy offsets in index
+// order.
 // ===========================================================================
 constexpr int K1_THREADS = 256;
 constexpr int K1_ROWS = 16;
@@ -178,53 +182,40 @@ __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long
     *reinterpret_cast<volatile unsigned long long*>(p) = v;
 }
 
-__global__ void __launch_bounds__(K1_THREADS)
-k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
-            unsigned long long* status, uint32_t* __restrict__ lidx, double* __restrict__ lw,
-            uint32_t* __restrict__ hidx, double* __restrict__ hw) {
-    extern __shared__ __align__(16) unsigned char k1_smem[];
-    double* sw = reinterpret_cast<double*>(k1_smem);                     // K1_TILE
-    uint32_t* sidx = reinterpret_cast<uint32_t*>(sw + K1_TILE);          // K1_TILE
-    uint32_t* cntL = sidx + K1_TILE;                                     // K1_SLOTS
-    uint32_t* cntH = cntL + K1_SLOTS;                                    // K1_SLOTS
-    __shared__ unsigned s_tile;
-    __shared__ unsigned long long s_excl;
-    __shared__ uint32_t s_totL, s_totH;
+struct TileCells {
+    uint32_t lm[K1_SLOTS], hm[K1_SLOTS];      // ballots per (row, warp)
+    uint32_t exL[K1_SLOTS], exH[K1_SLOTS];    // exclusive offsets per cell
+    uint32_t totL, totH;
+};
 
+// Loads the tile's weights into xs (when KEEP), fills cells (ballots, offsets,
+// totals).  Ends with __syncthreads().
+template <bool KEEP>
+__device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint64_t n,
+                                              uint64_t base, double wn, double* xs,
+                                              TileCells& C) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(&sc->tile_counter, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    const uint64_t base = tile * K1_TILE;
-    const double wn = __ldcg(&sc->wn);
-
-    double xs[K1_ROWS];
-    unsigned lm[K1_ROWS], hm[K1_ROWS];
 #pragma unroll
     for (int r = 0; r < K1_ROWS; ++r) {
         const uint64_t gi = base + r * K1_THREADS + tid;
-        xs[r] = gi < n ? __ldg(w + gi) : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < K1_ROWS; ++r) {
-        const uint64_t gi = base + r * K1_THREADS + tid;
+        const double x = gi < n ? __ldg(w + gi) : 0.0;
+        if (KEEP) xs[r] = x;
         const bool valid = gi < n;
-        const bool light = valid && xs[r] <= wn;  // ties are light (alias.hpp:60)
-        lm[r] = __ballot_sync(0xffffffffu, light);
-        hm[r] = __ballot_sync(0xffffffffu, valid && !light);
+        const bool light = valid && x <= wn;  // ties are light (alias.hpp:60)
+        const unsigned lm = __ballot_sync(0xffffffffu, light);
+        const unsigned hm = __ballot_sync(0xffffffffu, valid && !light);
         if (lane == 0) {
-            cntL[r * 8 + warp] = __popc(lm[r]);
-            cntH[r * 8 + warp] = __popc(hm[r]);
+            C.lm[r * 8 + warp] = lm;
+            C.hm[r * 8 + warp] = hm;
         }
     }
     __syncthreads();
     if (warp == 0) {
-        // exclusive scans over the 128 (row, warp) cells in index order
         uint32_t a[4], b[4], sa = 0, sb = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            a[q] = cntL[lane * 4 + q];
-            b[q] = cntH[lane * 4 + q];
+            a[q] = __popc(C.lm[lane * 4 + q]);
+            b[q] = __popc(C.hm[lane * 4 + q]);
             sa += a[q];
             sb += b[q];
         }
@@ -241,14 +232,47 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
         uint32_t ea = ia - sa, eb = ib - sb;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            cntL[lane * 4 + q] = ea;
-            cntH[lane * 4 + q] = eb;
+            C.exL[lane * 4 + q] = ea;
+            C.exH[lane * 4 + q] = eb;
             ea += a[q];
             eb += b[q];
         }
-        const uint32_t totL = __shfl_sync(0xffffffffu, ia, 31);
-        const uint32_t totH = __shfl_sync(0xffffffffu, ib, 31);
+        if (lane == 31) {
+            C.totL = ia;
+            C.totH = ib;
+        }
+    }
+    __syncthreads();
+}
 
+// ===========================================================================
+// K1: stable light/heavy partition with decoupled look-back
+//   in : w (8 B/item)
+//   out: light weights lw (list order), heavy ids + weights hidx/hw.
+//   The light ids are never materialised: K4b recovers them from the tile
+//   prefix counts this kernel leaves in `status`.
+// ===========================================================================
+__global__ void __launch_bounds__(K1_THREADS)
+k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
+            unsigned long long* status, double* __restrict__ lw, uint32_t* __restrict__ hidx,
+            double* __restrict__ hw) {
+    extern __shared__ __align__(16) unsigned char k1_smem[];
+    double* sw = reinterpret_cast<double*>(k1_smem);              // K1_TILE
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(sw + K1_TILE);   // K1_TILE
+    __shared__ TileCells C;
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_excl;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(&sc->tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * K1_TILE;
+    double xs[K1_ROWS];
+    classify_tile<true>(w, n, base, __ldcg(&sc->wn), xs, C);
+
+    if (warp == 0) {
+        const uint32_t totL = C.totL;
         // decoupled look-back for the number of lights before this tile
         unsigned long long excl = 0;
         if (tile == 0) {
@@ -280,8 +304,6 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
         }
         if (lane == 0) {
             s_excl = excl;
-            s_totL = totL;
-            s_totH = totH;
             if (tile + 1 == ntiles) {
                 sc->nl = excl + totL;
                 sc->nh = n - (excl + totL);
@@ -289,27 +311,23 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
         }
     }
     __syncthreads();
-    const uint32_t totL = s_totL, totH = s_totH;
+    const uint32_t totL = C.totL, totH = C.totH;
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int r = 0; r < K1_ROWS; ++r) {
-        const uint64_t gi = base + r * K1_THREADS + tid;
-        if ((lm[r] >> lane) & 1) {
-            const uint32_t p = cntL[r * 8 + warp] + __popc(lm[r] & lt);
-            sidx[p] = static_cast<uint32_t>(gi);
-            sw[p] = xs[r];
-        } else if ((hm[r] >> lane) & 1) {
-            const uint32_t p = totL + cntH[r * 8 + warp] + __popc(hm[r] & lt);
-            sidx[p] = static_cast<uint32_t>(gi);
+        const int cell = r * 8 + warp;
+        const unsigned lm = C.lm[cell], hm = C.hm[cell];
+        if ((lm >> lane) & 1) {
+            sw[C.exL[cell] + __popc(lm & lt)] = xs[r];
+        } else if ((hm >> lane) & 1) {
+            const uint32_t p = totL + C.exH[cell] + __popc(hm & lt);
+            sidx[p] = static_cast<uint32_t>(base + r * K1_THREADS + threadIdx.x);
             sw[p] = xs[r];
         }
     }
     __syncthreads();
     const uint64_t L0 = s_excl, H0 = base - s_excl;
-    for (uint32_t p = tid; p < totL; p += K1_THREADS) {
-        lidx[L0 + p] = sidx[p];
-        lw[L0 + p] = sw[p];
-    }
+    for (uint32_t p = tid; p < totL; p += K1_THREADS) lw[L0 + p] = sw[p];
     for (uint32_t p = tid; p < totH; p += K1_THREADS) {
         hidx[H0 + p] = sidx[totL + p];
         hw[H0 + p] = sw[totL + p];
@@ -406,13 +424,16 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
 
 // ===========================================================================
 // K2b: serial carry chain over the block totals (parallel.hpp:116-121)
+//   One lane per list runs the inherently sequential Neumaier chain; the rest
+//   of the warp streams the totals into shared memory ahead of it.  The loop
+//   is unrolled so smem loads and carry stores leave the dependent DADD chain.
 // ===========================================================================
 constexpr int K2B_CHUNK = 1024;
 
 __global__ void __launch_bounds__(32)
 k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* carries,
              double* lpre, double* hpre) {
-    __shared__ double buf[2][K2B_CHUNK];
+    __shared__ __align__(16) double buf[2][K2B_CHUNK];
     const int lane = threadIdx.x;
     const uint64_t nl = sc->nl, nh = sc->nh;
     const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
@@ -445,9 +466,24 @@ k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* ca
         __syncwarp();
         if (lane == 0) {
             const int cnt = static_cast<int>(umin64(K2B_CHUNK, nb - c * K2B_CHUNK));
-            for (int i = 0; i < cnt; ++i) {
-                const double t = buf[bsel][i];
-                dst[c * K2B_CHUNK + i] = acc.value();
+            double* out = dst + c * K2B_CHUNK;
+            const double* in = buf[bsel];
+            int i = 0;
+            for (; i + 16 <= cnt; i += 16) {
+                double t[16], v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) t[u] = in[i + u];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    v[u] = acc.value();  // carry[b] = acc.value(), then acc.add(total)
+                    acc.add(t[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) out[i + u] = v[u];
+            }
+            for (; i < cnt; ++i) {
+                const double t = in[i];
+                out[i] = acc.value();
                 acc.add(t);
             }
         }
@@ -503,44 +539,43 @@ k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__
 }
 
 // ===========================================================================
-// K4: pack (psa_pack, alias.hpp:160-209) -- one lane per job
+// K4a: pack (psa_pack, alias.hpp:160-209) -- one lane per job
+//   Each lane runs its job's sequential compensated sweep.  Work proceeds in
+//   phases of K4_S steps; before a phase the warp stages, for every lane, the
+//   next K4_S light weights and K4_S+1 heavy (weight, id) pairs with
+//   coalesced async copies, and after it flushes what the lanes produced in
+//   LIST order: the alias of every light and the (share, alias) of every
+//   heavy.  K4b turns those into index-ordered 16-B buckets with full-line
+//   stores (scattered 16-B bucket stores here would be half-sector writes,
+//   which the ECC-protected HBM turns into read-modify-writes).
 // ===========================================================================
 constexpr int K4_S = 32;      // steps per phase (= max items consumed per list)
 constexpr int K4_WARPS = 2;
-constexpr int K4_LW = K4_S + 1;   // light window row stride
+constexpr int K4_LW = K4_S + 1;   // light window row stride (odd -> no bank conflicts)
 constexpr int K4_HW = K4_S + 2;   // heavy window row stride (S + 1 lookahead)
 
 enum : int { ST_MAIN = 0, ST_TAILA = 1, ST_TAILB = 2, ST_DONE = 3 };
 
 struct K4Smem {
-    double lw[32][K4_LW];
-    uint32_t lix[32][K4_LW];
-    uint32_t lal[32][K4_LW];
-    double hw[32][K4_HW];
-    uint32_t hix[32][K4_HW];
-    uint32_t hal[32][K4_HW];
+    double lw[32][K4_LW];     // light weight in, light alias (low word) out
+    double hw[32][K4_HW];     // heavy weight in, heavy share out
+    uint32_t hix[32][K4_HW];  // heavy id in, heavy alias out
 };
 
+__device__ __forceinline__ uint32_t& low_word(double& d) { return reinterpret_cast<uint32_t*>(&d)[0]; }
+
 __global__ void __launch_bounds__(K4_WARPS * 32)
-k_pack(uint64_t n, uint64_t P, const double* __restrict__ w, DevScalars* sc,
-       const uint32_t* __restrict__ lidx, const double* __restrict__ lw,
+k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
        const uint32_t* __restrict__ hidx, const double* __restrict__ hw,
        const uint32_t* __restrict__ split_l, const uint32_t* __restrict__ split_h,
-       const double* __restrict__ split_s, Bucket* __restrict__ out) {
+       const double* __restrict__ split_s, uint32_t* __restrict__ lalias,
+       double* __restrict__ hshare, uint32_t* __restrict__ halias) {
     extern __shared__ __align__(16) unsigned char k4_smem[];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     K4Smem& S = reinterpret_cast<K4Smem*>(k4_smem)[wq];
     const uint64_t nh = sc->nh;
+    if (nh == 0) return;  // all items tie with the mean: K4b fills (alias.hpp:288-297)
     const double wn = sc->wn;
-
-    if (nh == 0) {
-        // fill_uniform_if_no_heavy (alias.hpp:288-297): every bucket keeps its item
-        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-             i += stride)
-            store_bucket(out, i, w[i], static_cast<uint32_t>(i), static_cast<uint32_t>(i));
-        return;
-    }
 
     const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * K4_WARPS + wq) * 32 + lane;
     uint64_t i = 0, lhi = 0, j = 0, hhi = 0;
@@ -560,12 +595,12 @@ k_pack(uint64_t n, uint64_t P, const double* __restrict__ w, DevScalars* sc,
     }
 
     while (__any_sync(0xffffffffu, state != ST_DONE)) {
-        // ---- windows for this phase --------------------------------------
+        // ---- stage this phase's windows ------------------------------------
         const bool live = state != ST_DONE;
         const uint64_t wl0 = i;
         const int lcnt = live ? static_cast<int>(umin64(K4_S, lhi - i)) : 0;
-        const uint64_t wh0 = min(j, nh - 1);
-        const uint64_t hend = min(min(j + K4_S + 1, hhi + 1), nh);
+        const uint64_t wh0 = umin64(j, nh - 1);
+        const uint64_t hend = umin64(umin64(j + K4_S + 1, hhi + 1), nh);
         const int hcnt = live ? static_cast<int>(hend - wh0) : 0;
 #pragma unroll 4
         for (int r = 0; r < 32; ++r) {
@@ -573,10 +608,7 @@ k_pack(uint64_t n, uint64_t P, const double* __restrict__ w, DevScalars* sc,
             const int rlc = __shfl_sync(0xffffffffu, lcnt, r);
             const uint64_t rh0 = __shfl_sync(0xffffffffu, wh0, r);
             const int rhc = __shfl_sync(0xffffffffu, hcnt, r);
-            if (lane < rlc) {
-                cp_async8(&S.lw[r][lane], lw + rl0 + lane);
-                cp_async4(&S.lix[r][lane], lidx + rl0 + lane);
-            }
+            if (lane < rlc) cp_async8(&S.lw[r][lane], lw + rl0 + lane);
             if (lane < rhc) {
                 cp_async8(&S.hw[r][lane], hw + rh0 + lane);
                 cp_async4(&S.hix[r][lane], hidx + rh0 + lane);
@@ -590,91 +622,134 @@ k_pack(uint64_t n, uint64_t P, const double* __restrict__ w, DevScalars* sc,
         cp_async_wait<0>();
         __syncwarp();
 
-        // ---- S sequential steps per lane ----------------------------------
+        // ---- up to K4_S sequential steps per lane ---------------------------
+        // Branch-free: every lane evaluates the same instruction stream, the
+        // operation (light bucket / heavy bucket / none) is a predicate.
+        // Window-relative 32-bit cursors: li = i - wl0, hj = j - wh0.
         const uint64_t i0 = i, j0 = j;
+        const int lrem = live ? static_cast<int>(umin64(lhi - i, K4_S + 1)) : 0;  // i < lhi
+        const int hrem = live ? static_cast<int>(umin64(hhi - wh0, K4_S + 2)) : 0; // j < hhi
+        const int hlast = static_cast<int>(umin64(nh - 1 - wh0, K4_S + 2));        // j+1 < nh
+        int li = 0, hj = static_cast<int>(j - wh0);
         double cLw = S.lw[lane][0];
-        uint32_t cLix = S.lix[lane][0];
         uint32_t hCur = S.hix[lane][0];  // heavy_at(j): slot of min(j, nh-1) = wh0
-        int qn = static_cast<int>(min(j + 1, nh - 1) - wh0);
+        int qn = min(min(hj + 1, hlast), K4_HW - 1);
         uint32_t hNext = S.hix[lane][qn];
         double hNextW = S.hw[lane][qn];
+#pragma unroll 2
         for (int step = 0; step < K4_S; ++step) {
-            if (state == ST_DONE) break;
             const double v = rem.value();
-            if (state == ST_MAIN) {
-                if (v > wn) {
-                    if (i >= lhi) state = ST_TAILA;
-                } else {
-                    if (j >= hhi) state = ST_TAILB;
-                }
+            const bool gt = v > wn;
+            const bool lightsLeft = li < lrem, heaviesLeft = hj < hrem;
+            int st = state;
+            if (st == ST_MAIN && gt && !lightsLeft) st = ST_TAILA;   // alias.hpp:172
+            if (st == ST_MAIN && !gt && !heaviesLeft) st = ST_TAILB; // alias.hpp:191
+            const bool isMain = st == ST_MAIN;
+            const bool lightOp = (isMain && gt) || (st == ST_TAILB && lightsLeft);
+            const bool heavyOp = (isMain && !gt) || (st == ST_TAILA && heaviesLeft);
+            if (!lightOp && !heavyOp) st = ST_DONE;  // tail loops exhausted: return
+            state = st;
+            // remainder update: rem.add(w - wn), or the reset at the last heavy
+            const bool hasNext = hj < hlast;
+            const double d = (lightOp ? cLw : hNextW) - wn;
+            const bool doAdd = (lightOp && isMain) || (heavyOp && hasNext);
+            const bool doReset = heavyOp && !hasNext;
+            CompSum nr = rem;
+            nr.add(d);
+            const double resetHi = isMain ? CUDART_INF : wn;  // rem = {inf} / rem = {wn}
+            rem.hi = doAdd ? nr.hi : (doReset ? resetHi : rem.hi);
+            rem.lo = doAdd ? nr.lo : (doReset ? 0.0 : rem.lo);
+            // light bucket {w, {idx, heavy_at(j)}} (alias.hpp:186-189, 194-197)
+            if (lightOp) low_word(S.lw[lane][li]) = hCur;
+            // heavy bucket {clamp(rem), {idx, heavy_at(j+1)}} (alias.hpp:175-183, 200-206)
+            if (heavyOp) {
+                S.hw[lane][hj] = isMain ? std_max(0.0, std_min(v, wn)) : std_min(v, wn);
+                S.hix[lane][hj] = hNext;
             }
-            bool lightOp, addL = false;
-            if (state == ST_MAIN) {
-                lightOp = v > wn;
-                addL = lightOp;
-            } else if (state == ST_TAILA) {
-                if (j >= hhi) {
-                    state = ST_DONE;
-                    break;
-                }
-                lightOp = false;
-            } else {  // ST_TAILB
-                if (i >= lhi) {
-                    state = ST_DONE;
-                    break;
-                }
-                lightOp = true;
-            }
-            if (lightOp) {
-                // buckets[idx] = {w, {idx, heavy_at(j)}} (alias.hpp:186-189, 194-197)
-                const int p = static_cast<int>(i - wl0);
-                S.lal[lane][p] = hCur;
-                if (addL) rem.add(cLw - wn);
-                ++i;
-                const int pn = min(p + 1, K4_S - 1);
-                cLw = S.lw[lane][pn];
-                cLix = S.lix[lane][pn];
-            } else {
-                // buckets[idx] = {clamp(rem), {idx, heavy_at(j+1)}} (alias.hpp:175-183, 200-206)
-                const int p = static_cast<int>(j - wh0);
-                const double share = state == ST_MAIN ? std_max(0.0, std_min(v, wn)) : std_min(v, wn);
-                S.hw[lane][p] = share;
-                S.hal[lane][p] = hNext;
-                if (j + 1 < nh) {
-                    rem.add(hNextW - wn);
-                } else {
-                    rem.hi = state == ST_MAIN ? CUDART_INF : wn;
-                    rem.lo = 0.0;
-                }
-                ++j;
+            li += lightOp;
+            hj += heavyOp;
+            if (lightOp) cLw = S.lw[lane][min(li, K4_S - 1)];
+            if (heavyOp) {
                 hCur = hNext;
-                qn = min(static_cast<int>(min(j + 1, nh - 1) - wh0), K4_HW - 1);
+                qn = min(min(hj + 1, hlast), K4_HW - 1);
                 hNext = S.hix[lane][qn];
                 hNextW = S.hw[lane][qn];
             }
         }
-        (void)cLix;
+        i = wl0 + li;
+        j = wh0 + hj;
         __syncwarp();
 
-        // ---- flush this phase's buckets ------------------------------------
+        // ---- flush this phase's outputs in list order ----------------------
         const int nlw = static_cast<int>(i - i0);
         const int nhw = static_cast<int>(j - j0);
         const int hoff = static_cast<int>(j0 - wh0);
 #pragma unroll 2
         for (int r = 0; r < 32; ++r) {
+            const uint64_t rl0 = __shfl_sync(0xffffffffu, i0, r);
+            const uint64_t rj0 = __shfl_sync(0xffffffffu, j0, r);
             const int rl = __shfl_sync(0xffffffffu, nlw, r);
             const int rh = __shfl_sync(0xffffffffu, nhw, r);
             const int ro = __shfl_sync(0xffffffffu, hoff, r);
-            if (lane < rl) {
-                const uint32_t idx = S.lix[r][lane];
-                store_bucket(out, idx, S.lw[r][lane], idx, S.lal[r][lane]);
-            }
+            if (lane < rl) lalias[rl0 + lane] = low_word(S.lw[r][lane]);
             if (lane < rh) {
-                const uint32_t idx = S.hix[r][ro + lane];
-                store_bucket(out, idx, S.hw[r][ro + lane], idx, S.hal[r][ro + lane]);
+                hshare[rj0 + lane] = S.hw[r][ro + lane];
+                halias[rj0 + lane] = S.hix[r][ro + lane];
             }
         }
         __syncwarp();
+    }
+}
+
+// ===========================================================================
+// K4b: assemble the 16-B buckets in index order (one CTA per K1 tile)
+//   light item i : {w_i, i, lalias[light rank]}      (alias.hpp:186-197)
+//   heavy item i : {hshare[rank], i, halias[rank]}   (alias.hpp:175-206)
+//   no heavy at all: {w_i, i, i}                     (alias.hpp:288-297)
+//   Ranks come from the same tile classification as K1 plus K1's inclusive
+//   tile prefix; every warp stores 32 consecutive buckets = 512 contiguous B.
+// ===========================================================================
+__global__ void __launch_bounds__(K1_THREADS)
+k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
+           const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lalias,
+           const double* __restrict__ hshare, const uint32_t* __restrict__ halias,
+           Bucket* __restrict__ out) {
+    __shared__ TileCells C;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t tile = blockIdx.x;
+    const uint64_t base = tile * K1_TILE;
+    const bool uniform = sc->nh == 0;
+    classify_tile<false>(w, n, base, sc->wn, nullptr, C);
+    const uint64_t L0 = (status[tile] & VAL_MASK) - C.totL;
+    const uint64_t H0 = base - L0;
+    const unsigned lt = lanemask_lt();
+    // Two half-tiles: issue all loads of 8 rows, then their 8 stores, so each
+    // thread has 8 independent gathers in flight.
+#pragma unroll
+    for (int h = 0; h < K1_ROWS; h += 8) {
+        double share[8];
+        uint32_t alias[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int r = h + u;
+            const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
+            const int cell = r * 8 + warp;
+            const unsigned lm = C.lm[cell];
+            const bool light = (lm >> lane) & 1;
+            const uint64_t p = light ? L0 + C.exL[cell] + __popc(lm & lt)
+                                     : H0 + C.exH[cell] + __popc(C.hm[cell] & lt);
+            share[u] = 0.0;
+            alias[u] = static_cast<uint32_t>(gi);
+            if (gi < n) {
+                share[u] = light ? __ldg(w + gi) : __ldg(hshare + p);
+                if (!uniform) alias[u] = light ? __ldg(lalias + p) : __ldg(halias + p);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint64_t gi = base + (h + u) * K1_THREADS + threadIdx.x;
+            if (gi < n) store_bucket(out, gi, share[u], static_cast<uint32_t>(gi), alias[u]);
+        }
     }
 }
 
@@ -687,7 +762,15 @@ static int k0_depth(uint64_t n) {
     return D;
 }
 
-cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P) {
+template <typename T>
+static cudaError_t ws_alloc(Workspace& ws, T*& ptr, uint64_t count) {
+    const uint64_t by = count * sizeof(T) + 64;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ptr), by);
+    if (e == cudaSuccess) ws.bytes += by;
+    return e;
+}
+
+cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate_outputs) {
     workspace_free(ws);
     ws.n = n;
     ws.P = P;
@@ -696,76 +779,81 @@ cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P) {
     const uint64_t cnts = (1ull << ws.k0_depth);
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 2;
-    cudaError_t e;
-#define WS_ALLOC(ptr, count)                                                         \
-    do {                                                                             \
-        const uint64_t by_ = static_cast<uint64_t>(count) * sizeof(*(ptr)) + 64;     \
-        e = cudaMalloc(reinterpret_cast<void**>(&(ptr)), by_);                       \
-        if (e != cudaSuccess) {                                                      \
-            workspace_free(ws);                                                      \
-            return e;                                                                \
-        }                                                                            \
-        ws.bytes += by_;                                                             \
-    } while (0)
-    WS_ALLOC(ws.node_val, nodes);
-    WS_ALLOC(ws.node_cnt, cnts);
-    WS_ALLOC(ws.tile_status, ntiles);
-    WS_ALLOC(ws.lidx, n);
-    WS_ALLOC(ws.hidx, n);
-    WS_ALLOC(ws.lw, n);
-    WS_ALLOC(ws.hw, n);
-    WS_ALLOC(ws.lpre, n + 1);
-    WS_ALLOC(ws.hpre, n + 1);
-    WS_ALLOC(ws.totals, nblocks);
-    WS_ALLOC(ws.carries, nblocks);
-    WS_ALLOC(ws.split_l, P + 1);
-    WS_ALLOC(ws.split_h, P + 1);
-    WS_ALLOC(ws.split_s, P + 1);
-    WS_ALLOC(ws.sc, 1);
-#undef WS_ALLOC
-    return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    auto A = [&](auto*& p, uint64_t c) {
+        if (e == cudaSuccess) e = ws_alloc(ws, p, c);
+    };
+    A(ws.node_val, nodes);
+    A(ws.node_cnt, cnts);
+    A(ws.tile_status, ntiles);
+    A(ws.hidx, n);
+    A(ws.lw, n);
+    A(ws.hw, n);
+    A(ws.lpre, n + 1);
+    A(ws.hpre, n + 1);
+    A(ws.halias, n);
+    A(ws.totals, nblocks);
+    A(ws.carries, nblocks);
+    A(ws.split_l, P + 1);
+    A(ws.split_h, P + 1);
+    A(ws.split_s, P + 1);
+    A(ws.sc, 1);
+    if (separate_outputs) {
+        A(ws.lalias_own, n);
+        A(ws.hshare_own, n);
+        ws.lalias = ws.lalias_own;
+        ws.hshare = ws.hshare_own;
+    } else {
+        // K4a runs after K3, the last reader of the prefix arrays: reuse them.
+        ws.lalias = reinterpret_cast<uint32_t*>(ws.lpre);
+        ws.hshare = ws.hpre;
+    }
+    if (e != cudaSuccess) workspace_free(ws);
+    return e;
 }
 
 cudaError_t workspace_alloc_total(Workspace& ws, uint64_t n) {
     workspace_free(ws);
     ws.n = n;
     ws.k0_depth = k0_depth(n);
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ws.node_val),
-                               ((2ull << ws.k0_depth) - 1) * sizeof(double));
-    if (e == cudaSuccess)
-        e = cudaMalloc(reinterpret_cast<void**>(&ws.node_cnt), (1ull << ws.k0_depth) * sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&ws.sc), sizeof(DevScalars));
+    cudaError_t e = ws_alloc(ws, ws.node_val, (2ull << ws.k0_depth) - 1);
+    if (e == cudaSuccess) e = ws_alloc(ws, ws.node_cnt, 1ull << ws.k0_depth);
+    if (e == cudaSuccess) e = ws_alloc(ws, ws.sc, 1);
     if (e != cudaSuccess) workspace_free(ws);
     return e;
 }
 
 void workspace_free(Workspace& ws) {
-    void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.lidx,    ws.hidx,
-                    ws.lw,       ws.hw,       ws.lpre,        ws.hpre,    ws.totals,
-                    ws.carries,  ws.split_l,  ws.split_h,     ws.split_s, ws.sc};
+    void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.hidx,       ws.lw,
+                    ws.hw,       ws.lpre,     ws.hpre,        ws.halias,     ws.totals,
+                    ws.carries,  ws.split_l,  ws.split_h,     ws.split_s,    ws.sc,
+                    ws.lalias_own, ws.hshare_own};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     ws = Workspace{};
 }
 
-static cudaError_t reset_scalars(Workspace& ws, cudaStream_t st) {
-    DevScalars init{};
-    init.bad_index = ~0ull;
-    // DevScalars is tiny: one async H2D from a constant pinned pattern is
-    // cheaper than several memsets, and the source outlives every copy.
-    static DevScalars* pinned = [&] {
+// DevScalars is tiny: one async H2D from a pinned per-device staging slot.
+static cudaError_t reset_scalars(Workspace& ws, cudaStream_t st, double total, double wn) {
+    constexpr int kSlots = 64;  // ring of pinned slots; a slot is reused 64 builds later
+    static DevScalars* pinned = [] {
         DevScalars* p = nullptr;
-        if (cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(DevScalars)) != cudaSuccess)
+        if (cudaMallocHost(reinterpret_cast<void**>(&p), kSlots * sizeof(DevScalars)) != cudaSuccess)
             return static_cast<DevScalars*>(nullptr);
-        *p = init;
         return p;
     }();
+    static std::atomic<unsigned> next{0};
     if (!pinned) return cudaErrorMemoryAllocation;
-    return cudaMemcpyAsync(ws.sc, pinned, sizeof(DevScalars), cudaMemcpyHostToDevice, st);
+    DevScalars* slot = pinned + (next.fetch_add(1) % kSlots);
+    *slot = DevScalars{};
+    slot->bad_index = ~0ull;
+    slot->total = total;
+    slot->wn = wn;
+    return cudaMemcpyAsync(ws.sc, slot, sizeof(DevScalars), cudaMemcpyHostToDevice, st);
 }
 
 cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStream_t st) {
-    cudaError_t e = reset_scalars(ws, st);
+    cudaError_t e = reset_scalars(ws, st, 0.0, 0.0);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(ws.node_cnt, 0, sizeof(unsigned) << ws.k0_depth, st);
     if (e != cudaSuccess) return e;
@@ -774,9 +862,9 @@ cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStrea
     return cudaGetLastError();
 }
 
-cudaError_t launch_psa_build(const double* d_w, uint64_t n, uint64_t P, Bucket* d_b,
-                             Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
-    const int k1_smem = K1_TILE * 12 + 2 * K1_SLOTS * 4;
+cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
+                             Bucket* d_b, Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
+    const int k1_smem = K1_TILE * 12;
     const int k4_smem = K4_WARPS * static_cast<int>(sizeof(K4Smem));
     // per-device attribute; cheap enough to set on every build
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
@@ -791,29 +879,32 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, uint64_t P, Bucket* 
     do {                                                \
         if (ev) cudaEventRecord(ev[i], st);             \
     } while (0)
-    REC(0);
-    e = launch_total(d_w, n, ws, st);
+    // bucket_mean_ = W / n (alias.hpp:247-248) with the weights' pairwise W
+    e = reset_scalars(ws, st, total, total / static_cast<double>(n));
     if (e != cudaSuccess) return e;
-    REC(1);
     e = cudaMemsetAsync(ws.tile_status, 0, ntiles * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
+    REC(0);
     k_partition<<<static_cast<unsigned>(ntiles), K1_THREADS, k1_smem, st>>>(
-        d_w, n, ntiles, ws.sc, ws.tile_status, ws.lidx, ws.lw, ws.hidx, ws.hw);
-    REC(2);
+        d_w, n, ntiles, ws.sc, ws.tile_status, ws.lw, ws.hidx, ws.hw);
+    REC(1);
     k_scan_blocks<false><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc,
                                                             ws.totals, ws.carries);
-    REC(3);
+    REC(2);
     k_scan_carry<<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
-    REC(4);
+    REC(3);
     k_scan_blocks<true><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc,
                                                            ws.totals, ws.carries);
-    REC(5);
+    REC(4);
     k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
                                      ws.split_s);
+    REC(5);
+    k_pack<<<k4_grid, K4_WARPS * 32, k4_smem, st>>>(P, ws.sc, ws.lw, ws.hidx, ws.hw, ws.split_l,
+                                                    ws.split_h, ws.split_s, ws.lalias, ws.hshare,
+                                                    ws.halias);
     REC(6);
-    k_pack<<<k4_grid, K4_WARPS * 32, k4_smem, st>>>(n, P, d_w, ws.sc, ws.lidx, ws.lw, ws.hidx,
-                                                    ws.hw, ws.split_l, ws.split_h, ws.split_s,
-                                                    d_b);
+    k_assemble<<<static_cast<unsigned>(ntiles), K1_THREADS, 0, st>>>(
+        d_w, n, ws.sc, ws.tile_status, ws.lalias, ws.hshare, ws.halias, d_b);
     REC(7);
 #undef REC
     return cudaGetLastError();

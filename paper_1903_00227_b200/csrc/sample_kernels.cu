@@ -1,81 +1,159 @@
 // paper_1903_00227_b200/csrc/sample_kernels.cu -- K5, bulk alias sampling,
 // plus the on-device uniform weight generator.
 //
-// K5 reproduces AliasTable::sample_many (alias.hpp:274-284) exactly: worker w
-// of W owns the contiguous output slice worker_slice(k, W, w)
+// Semantics: AliasTable::sample_many (alias.hpp:274-284) bit for bit.  Worker
+// w of W owns the contiguous output slice worker_slice(k, W, w)
 // (parallel.hpp:37-43) and draws it from RngStream(seed, 'alia').derive(w);
 // query m of a slice consumes outputs 2m+1 (bucket via the 128-bit
 // multiply-shift, rng.hpp:63-66) and 2m+2 (coin, rng.hpp:53-55) of that
-// counter stream, then returns ia[x >= share] (alias.hpp:265-269).  Because
-// the stream is counter-based every output position is computable on its own,
-// so the GPU assigns positions to threads freely and still matches the
-// reference bit for bit.
+// counter stream and returns ia[x >= share] (alias.hpp:265-269).  The stream
+// is counter-based, so every output position is computable on its own and the
+// GPU is free to choose WHEN it computes each one.
 //
-// Memory behaviour: one random 16-B bucket gather (one 32-B sector) plus one
-// coalesced 4-B store per sample.  Each thread keeps kUnroll independent
-// gathers in flight; outputs are written warp-contiguous.
+// Two execution plans:
+//   direct  (table L2-resident or few draws): one kernel, one 16-B gather per
+//           draw straight from the table.
+//   region  (table >> L2): measured on B200, every random 16-B gather from an
+//           HBM-resident table moves a full 128-B line (ncu: 126 B/draw), so
+//           the direct plan tops out near 6.5 TB/s / 132 B = 50 G draws/s.
+//           The region plan reorders the WORK, not the results: draws are
+//           bucketed by table region (2^21 buckets = 32 MB, L2-resident) with
+//           a stable counting sort, the gathers then sweep the table region by
+//           region so every line is fetched from HBM about once, and a final
+//           pass puts the answers back in output order.  Traffic per draw:
+//           8 B record write + 8 B read + 4 B result write + 4 B read + 4 B
+//           output write, plus 16n B of table per pass.
+//     RA  k_region_count    per-tile region histograms
+//     RS  k_scan_*          exclusive scan of the (region, tile) counts
+//     RB  k_region_scatter  (q, bucket) records in region-major order
+//     RC  k_region_gather   coin flip + bucket gather, region by region
+//     RD  k_region_unpermute out[q] = result[position of q]
+#include <cmath>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "engine.h"
 
 namespace wrsb {
 
-constexpr int K5_THREADS = 256;
-constexpr int K5_UNROLL = 8;
+// ===========================================================================
+// shared: where query q lives in the worker partition, and its two draws
+// ===========================================================================
+struct DrawGeom {
+    uint64_t n;         // buckets
+    double wn;          // bucket mean W/n
+    uint64_t base_key;  // RngStream(seed, stream).key
+    uint64_t k;         // total draws of the call (defines worker slices)
+    uint32_t W;         // workers
+    uint64_t per, rem, big;  // k/W, k%W, rem*(per+1)
+    double inv_p1, inv_p;    // 1/(per+1), 1/per for the division estimate
+};
+
+DrawGeom make_geom(uint64_t n, double wn, uint64_t seed, uint64_t stream_id, uint64_t k,
+                   uint32_t W) {
+    DrawGeom g{};
+    g.n = n;
+    g.wn = wn;
+    g.base_key = rng_key(seed, stream_id);
+    g.k = k;
+    g.W = W ? W : 1;
+    g.per = k / g.W;
+    g.rem = k % g.W;
+    g.big = g.rem * (g.per + 1);
+    g.inv_p1 = 1.0 / static_cast<double>(g.per + 1);
+    g.inv_p = g.per ? 1.0 / static_cast<double>(g.per) : 0.0;
+    return g;
+}
+
+// floor(a / d) for a < 2^53 from a double estimate plus exact correction.
+__device__ __forceinline__ uint64_t div_est(uint64_t a, uint64_t d, double inv) {
+    uint64_t t = static_cast<uint64_t>(static_cast<double>(a) * inv);
+    while (t * d > a) --t;
+    while ((t + 1) * d <= a) ++t;
+    return t;
+}
+
+// worker_slice inverse (parallel.hpp:37-43): q -> (worker, index in slice).
+__device__ __forceinline__ void locate(const DrawGeom& g, uint64_t q, uint32_t& w, uint64_t& m) {
+    if (g.W == 1) {
+        w = 0;
+        m = q;
+    } else if (q < g.big) {
+        const uint64_t t = div_est(q, g.per + 1, g.inv_p1);
+        w = static_cast<uint32_t>(t);
+        m = q - t * (g.per + 1);
+    } else {
+        const uint64_t r = q - g.big;
+        const uint64_t t = div_est(r, g.per, g.inv_p);
+        w = static_cast<uint32_t>(g.rem + t);
+        m = r - t * g.per;
+    }
+}
+
+// Per-thread cache of the last worker's derived key.
+struct KeyCache {
+    uint32_t w = 0xffffffffu;
+    uint64_t key = 0;
+    __device__ __forceinline__ uint64_t get(const DrawGeom& g, uint32_t wk) {
+        if (wk != w) {
+            w = wk;
+            key = rng_derive(g.base_key, wk);  // RngStream(...).derive(worker), alias.hpp:280
+        }
+        return key;
+    }
+};
+
+// bounded(n) of output 2m+1 (rng.hpp:63-66)
+__device__ __forceinline__ uint64_t draw_bucket(const DrawGeom& g, uint64_t key, uint64_t m) {
+    return __umul64hi(mix64(key + (2 * m + 1) * kGolden), g.n);
+}
+// uniform01() * bucket_mean of output 2m+2 (rng.hpp:53-55, alias.hpp:267)
+__device__ __forceinline__ double draw_coin(const DrawGeom& g, uint64_t key, uint64_t m) {
+    const uint64_t r = mix64(key + (2 * m + 2) * kGolden);
+    return (static_cast<double>(r >> 11) * 0x1.0p-53) * g.wn;
+}
 
 __device__ __forceinline__ uint4 ld_bucket(const Bucket* b, uint64_t i) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(b + i));
     return v;
 }
+__device__ __forceinline__ uint32_t pick(const uint4& bk, double x) {
+    const double share = __hiloint2double(static_cast<int>(bk.y), static_cast<int>(bk.x));
+    return x >= share ? bk.w : bk.z;  // ia[x >= share] (alias.hpp:268)
+}
 
-struct SliceCursor {
-    uint64_t per, rem, big;  // per = k/W, rem = k%W, big = rem*(per+1)
-    __device__ __forceinline__ uint32_t worker_of(uint64_t q) const {
-        return q < big ? static_cast<uint32_t>(q / (per + 1))
-                       : static_cast<uint32_t>(rem + (q - big) / per);
-    }
-    __device__ __forceinline__ uint64_t lo_of(uint32_t w) const {
-        return per * w + (w < rem ? w : rem);
-    }
-};
+// ===========================================================================
+// direct plan
+// ===========================================================================
+constexpr int K5_THREADS = 256;
+constexpr int K5_UNROLL = 8;
 
 __global__ void __launch_bounds__(K5_THREADS)
-k_sample(const Bucket* __restrict__ b, uint64_t n, double wn, uint64_t base_key, uint64_t k,
-         uint32_t W, uint64_t q_begin, uint64_t q_end, uint32_t out_base,
-         uint32_t* __restrict__ out) {
-    const SliceCursor sl{k / W, k % W, (k % W) * (k / W + 1)};
+k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_end,
+         uint32_t out_base, uint32_t* __restrict__ out) {
     const uint64_t span = static_cast<uint64_t>(K5_THREADS) * K5_UNROLL;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * span;
     out -= q_begin;  // out[q] for q in [q_begin, q_end)
+    KeyCache kc;
     for (uint64_t q0 = q_begin + static_cast<uint64_t>(blockIdx.x) * span + threadIdx.x;
          q0 < q_end; q0 += stride) {
-        // worker of the first query; later ones advance past slice ends
-        uint32_t w = sl.worker_of(q0);
-        uint64_t lo = sl.lo_of(w);
-        uint64_t hi = lo + sl.per + (w < sl.rem ? 1 : 0);
-        uint64_t key = rng_derive(base_key, w);
         uint64_t bidx[K5_UNROLL];
         double x[K5_UNROLL];
 #pragma unroll
         for (int u = 0; u < K5_UNROLL; ++u) {
             const uint64_t q = q0 + static_cast<uint64_t>(u) * K5_THREADS;
+            bidx[u] = 0;
+            x[u] = 0.0;
             if (q < q_end) {
-                while (q >= hi) {
-                    ++w;
-                    lo = hi;
-                    hi = lo + sl.per + (w < sl.rem ? 1 : 0);
-                    key = rng_derive(base_key, w);
-                }
-                const uint64_t m = q - lo;
-                const uint64_t r1 = mix64(key + (2 * m + 1) * kGolden);
-                const uint64_t r2 = mix64(key + (2 * m + 2) * kGolden);
-                bidx[u] = __umul64hi(r1, n);                              // bounded(n)
-                x[u] = (static_cast<double>(r2 >> 11) * 0x1.0p-53) * wn;  // uniform01()*wn
-            } else {
-                bidx[u] = 0;
-                x[u] = 0.0;
+                uint32_t w;
+                uint64_t m;
+                locate(g, q, w, m);
+                const uint64_t key = kc.get(g, w);
+                bidx[u] = draw_bucket(g, key, m);
+                x[u] = draw_coin(g, key, m);
             }
         }
         uint4 bk[K5_UNROLL];
@@ -84,15 +162,258 @@ k_sample(const Bucket* __restrict__ b, uint64_t n, double wn, uint64_t base_key,
 #pragma unroll
         for (int u = 0; u < K5_UNROLL; ++u) {
             const uint64_t q = q0 + static_cast<uint64_t>(u) * K5_THREADS;
-            if (q < q_end) {
-                const double share = __hiloint2double(static_cast<int>(bk[u].y),
-                                                      static_cast<int>(bk[u].x));
-                out[q] = (x[u] >= share ? bk[u].w : bk[u].z) + out_base;
-            }
+            if (q < q_end) out[q] = pick(bk[u], x[u]) + out_base;
         }
     }
 }
 
+
+// ===========================================================================
+// region plan
+//   Tiles of RS_TILE consecutive draws; warp w of a tile owns the RS_SUB
+//   consecutive draws [w*RS_SUB, (w+1)*RS_SUB) in rows of 32.  Inside a tile
+//   the draws are laid out by (region, warp, row, lane); each region's run of
+//   the tile moves to and from global memory as one contiguous block through
+//   shared memory.  Region r owns a fixed slab [r*cap, (r+1)*cap) of the
+//   record array; tiles claim space in it with one atomicAdd per (tile,
+//   region), so no counting pass is needed (the order of runs inside a slab
+//   is arbitrary and does not affect any result).  A run that would overflow
+//   its slab (cap has ~20 sigma of slack) goes to a shared overflow slab.
+// ===========================================================================
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ROWS = 16;                        // rows of 32 draws per warp
+constexpr int RS_TILE = RS_THREADS * RS_ROWS;      // 4096 draws per tile
+constexpr int RS_SUB = 32 * RS_ROWS;               // 512 consecutive draws per warp
+constexpr int RS_MAX_REGIONS = 1024;
+
+struct RegionGeom {
+    DrawGeom g;
+    uint64_t q0;       // first draw of this chunk
+    uint64_t kc;       // draws in this chunk
+    uint64_t ntiles;   // ceil(kc / RS_TILE)
+    uint32_t nreg;     // regions
+    int shift;         // region = bucket >> shift
+    uint32_t cap;      // records per region slab
+    uint32_t ov_cap;   // records in the overflow slab (after the nreg slabs)
+};
+
+// per (tile, region): global start of the tile's run and its tile-local start
+struct RunInfo {
+    uint32_t goff;
+    uint32_t loc;
+};
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint32_t* p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;"
+                 :: "l"(p), "r"(v), "l"(pol));
+}
+__device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(b + i), "l"(pol));
+    return v;
+}
+
+// RB: draws -> region slabs.  Each thread computes 16 draws' buckets and
+// claims a rank inside its region with a shared-memory atomic; a warp scan
+// turns the region counts into tile-local run starts; the (draw, bucket)
+// records are staged in shared memory in region order and each run is then
+// written to its slab as one contiguous block.  The tile slot of every draw
+// is recorded (q order) for RD, so the (non-deterministic) order inside a run
+// never needs to be reproduced.
+__host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg) {
+    const size_t head = (2 * static_cast<size_t>(nreg) + 1) * 4;
+    return ((head + 15) & ~size_t(15)) + RS_TILE * sizeof(uint2);
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restrict__ overflow,
+                 uint2* __restrict__ rec, uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    uint32_t* loc = reinterpret_cast<uint32_t*>(rs_smem);  // counts, then run starts
+    uint32_t* goff = loc + rg.nreg + 1;
+    uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((2 * rg.nreg + 1) * 4 + 15) & ~15u));
+    const uint64_t tile = blockIdx.x;
+    const uint64_t tbase = tile * RS_TILE;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i <= rg.nreg; i += RS_THREADS) loc[i] = 0;
+    __syncthreads();
+
+    uint32_t bk[RS_ROWS], rank[RS_ROWS];
+    KeyCache kc;
+#pragma unroll
+    for (int r = 0; r < RS_ROWS; ++r) {
+        const uint64_t qc = tbase + r * RS_THREADS + threadIdx.x;
+        bk[r] = 0xffffffffu;
+        rank[r] = 0;
+        if (qc < rg.kc) {
+            uint32_t w;
+            uint64_t m;
+            locate(rg.g, rg.q0 + qc, w, m);
+            bk[r] = static_cast<uint32_t>(draw_bucket(rg.g, kc.get(rg.g, w), m));
+            rank[r] = atomicAdd(&loc[bk[r] >> rg.shift], 1u);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the region counts, 32 at a time
+        uint32_t carry = 0;
+        for (uint32_t r0 = 0; r0 < rg.nreg; r0 += 32) {
+            const uint32_t reg = r0 + lane;
+            const uint32_t c = reg < rg.nreg ? loc[reg] : 0;
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (reg < rg.nreg) loc[reg] = carry + x - c;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) loc[rg.nreg] = carry;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ROWS; ++r) {
+        const uint64_t qc = tbase + r * RS_THREADS + threadIdx.x;
+        if (qc < rg.kc) {
+            const uint32_t slot = loc[bk[r] >> rg.shift] + rank[r];
+            stage[slot] = make_uint2(static_cast<uint32_t>(qc), bk[r]);
+            slot_of[qc] = static_cast<uint16_t>(slot);
+        }
+    }
+    // claim slab space for each non-empty run of this tile
+    for (uint32_t reg = threadIdx.x; reg < rg.nreg; reg += RS_THREADS) {
+        const uint32_t c = loc[reg + 1] - loc[reg];
+        uint32_t g = 0;
+        if (c) {
+            const uint32_t base = atomicAdd(&cursor[reg], c);
+            if (base + c <= rg.cap) {
+                g = reg * rg.cap + base;
+            } else {
+                const uint32_t ob = atomicAdd(&cursor[rg.nreg], c);
+                if (ob + c > rg.ov_cap) atomicOr(overflow, 1u);
+                g = rg.nreg * rg.cap + (ob + c <= rg.ov_cap ? ob : 0);
+            }
+        }
+        goff[reg] = g;
+        runs[tile * rg.nreg + reg] = RunInfo{g, loc[reg]};
+    }
+    __syncthreads();
+    if (*overflow) return;
+    const uint64_t pol = policy_evict_first();
+    for (uint32_t reg = warp; reg < rg.nreg; reg += RS_WARPS) {  // one run per warp
+        const uint32_t l0 = loc[reg], c = loc[reg + 1] - l0;
+        uint2* dst = rec + goff[reg];
+        for (uint32_t t = lane; t < c; t += 32) {
+            const uint2 v = stage[l0 + t];
+            asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
+                         :: "l"(dst + t), "r"(v.x), "r"(v.y), "l"(pol));
+        }
+    }
+}
+
+// RC: slab by slab, the coin flip of every record against its bucket.  One
+// contiguous run of 2048 slab positions per CTA, so the resident CTAs of the
+// GPU sweep the table region by region; table loads are marked evict-last,
+// record / result streams evict-first.
+__global__ void __launch_bounds__(256)
+k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
+                const uint2* __restrict__ rec, uint32_t* __restrict__ res) {
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 2048;
+    const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);  // nreg = overflow slab
+    const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
+    const uint64_t valid_end =
+        slab0 + (slab < rg.nreg ? umin64(cursor[slab], rg.cap) : umin64(cursor[rg.nreg], rg.ov_cap));
+    if (p0 >= valid_end) return;
+    const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+    KeyCache kc;
+    uint2 r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint64_t p = p0 + u * 256 + threadIdx.x;
+        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
+    }
+    uint4 bk[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bk[u] = ld_table(b, r[u].y, pl);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint64_t p = p0 + u * 256 + threadIdx.x;
+        if (p < valid_end) {
+            uint32_t w;
+            uint64_t m;
+            locate(rg.g, rg.q0 + r[u].x, w, m);
+            st_stream(res + p, pick(bk[u], draw_coin(rg.g, kc.get(rg.g, w), m)), pf);
+        }
+    }
+}
+
+// RD: results back to draw order.  Each region run of the tile is read as one
+// contiguous block into shared memory at its tile-local start; every draw
+// then picks its answer at the slot RB recorded for it.  If a slab ever
+// overflowed (not expected: ~20 sigma of slack), the tile recomputes its
+// draws directly instead, so the output is correct in every case.
+__global__ void __launch_bounds__(RS_THREADS)
+k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
+                   const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
+                   const uint16_t* __restrict__ slot_of, const uint32_t* __restrict__ res,
+                   uint32_t out_base, uint32_t* __restrict__ out) {
+    __shared__ uint32_t stage[RS_TILE];
+    const uint64_t tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t tbase = tile * RS_TILE;
+    const uint32_t tcount = static_cast<uint32_t>(umin64(RS_TILE, rg.kc - tbase));
+    if (*overflow) {
+        KeyCache kc;
+        for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS) {
+            uint32_t w;
+            uint64_t m;
+            locate(rg.g, rg.q0 + tbase + e, w, m);
+            const uint64_t key = kc.get(rg.g, w);
+            out[tbase + e] = pick(ld_bucket(b, draw_bucket(rg.g, key, m)), draw_coin(rg.g, key, m)) +
+                             out_base;
+        }
+        return;
+    }
+    const uint64_t pf = policy_evict_first();
+    const RunInfo* tr = runs + tile * rg.nreg;
+    for (uint32_t reg = warp; reg < rg.nreg; reg += RS_WARPS) {
+        const RunInfo ri = tr[reg];
+        const uint32_t l1 = reg + 1 < rg.nreg ? tr[reg + 1].loc : tcount;
+        for (uint32_t t = lane; t < l1 - ri.loc; t += 32)
+            stage[ri.loc + t] = ld_stream(res + ri.goff + t, pf);
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS)
+        out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
 __global__ void k_generate_uniform(double* __restrict__ w, uint64_t n, uint64_t offset,
                                    uint64_t key) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -111,18 +432,137 @@ static int sm_count() {
     return sms;
 }
 
+static int region_shift() { return 21; }  // 2^21 buckets = 32 MB per region
+
+bool use_region_plan(uint64_t n, uint64_t k) {
+    const uint64_t nreg = (n + (1ull << region_shift()) - 1) >> region_shift();
+    // table well beyond L2 and enough draws per bucket to reuse the lines
+    return n * sizeof(Bucket) > (96ull << 20) && k * 8 >= n && nreg <= RS_MAX_REGIONS;
+}
+
+struct RegionPlan {
+    RegionGeom rg;
+    uint64_t rec_slots;  // nreg * cap + ov_cap
+};
+
+static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
+    RegionPlan p{};
+    p.rg.g = g;
+    p.rg.shift = region_shift();
+    p.rg.nreg = static_cast<uint32_t>((g.n + (1ull << p.rg.shift) - 1) >> p.rg.shift);
+    // expected draws per full region + ~20 sigma + a tile of slack
+    const double mu = static_cast<double>(chunk) *
+                      (static_cast<double>(1ull << p.rg.shift) / static_cast<double>(g.n));
+    const double cap = mu + 20.0 * std::sqrt(mu) + 2.0 * RS_TILE;
+    // slabs are whole multiples of the gather CTA's 2048 positions
+    auto round2k = [](uint64_t x) { return static_cast<uint32_t>((x + 2047) & ~uint64_t(2047)); };
+    p.rg.cap = round2k(static_cast<uint64_t>(cap < static_cast<double>(chunk) ? cap : chunk) + RS_TILE);
+    p.rg.ov_cap = round2k(chunk / 64 + 8 * RS_TILE);
+    p.rec_slots = static_cast<uint64_t>(p.rg.nreg) * p.rg.cap + p.rg.ov_cap;
+    return p;
+}
+
+static uint64_t region_chunk_max() {
+    uint64_t chunk_max = 1ull << 30;  // draws per region pass
+    if (const char* env = getenv("WRS_B200_DRAW_CHUNK")) {
+        const unsigned long long v = strtoull(env, nullptr, 10);
+        if (v >= RS_TILE) chunk_max = v;
+    }
+    return chunk_max;
+}
+
+struct RegionBuffers {
+    uint2* rec;
+    uint32_t* res;
+    uint16_t* slot_of;
+    RunInfo* runs;
+    uint32_t* cursor;
+    unsigned* overflow;
+};
+
+static uint64_t region_bytes(const RegionPlan& p, uint64_t chunk, RegionBuffers* b, void* base) {
+    const uint64_t ntiles = (chunk + RS_TILE - 1) / RS_TILE;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t o = off;
+        off += (bytes + 255) & ~uint64_t(255);
+        return static_cast<char*>(base) + o;
+    };
+    char* rec = take(p.rec_slots * sizeof(uint2));
+    char* res = take(p.rec_slots * sizeof(uint32_t));
+    char* slot = take(chunk * sizeof(uint16_t));
+    char* runs = take(ntiles * p.rg.nreg * sizeof(RunInfo));
+    char* cur = take((p.rg.nreg + 1) * 4 + 4);
+    if (b) {
+        b->rec = reinterpret_cast<uint2*>(rec);
+        b->res = reinterpret_cast<uint32_t*>(res);
+        b->slot_of = reinterpret_cast<uint16_t*>(slot);
+        b->runs = reinterpret_cast<RunInfo*>(runs);
+        b->cursor = reinterpret_cast<uint32_t*>(cur);
+        b->overflow = reinterpret_cast<unsigned*>(cur) + p.rg.nreg + 1;
+    }
+    return off;
+}
+
+cudaError_t SampleWorkspace::reserve(uint64_t need) {
+    if (need <= bytes) return cudaSuccess;
+    release();
+    cudaError_t e = cudaMalloc(&base, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+}
+
+void SampleWorkspace::release() {
+    if (base) cudaFree(base);
+    base = nullptr;
+    bytes = 0;
+}
+
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
-                          uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st) {
+                          uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,
+                          SampleWorkspace* ws) {
     if (q_end <= q_begin) return cudaSuccess;
-    if (workers == 0) workers = 1;
-    const uint64_t span = static_cast<uint64_t>(K5_THREADS) * K5_UNROLL;
-    uint64_t blocks = (q_end - q_begin + span - 1) / span;
-    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8 * 64;  // grid-stride beyond this
-    if (blocks > cap) blocks = cap;
-    k_sample<<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(
-        d_b, n, wn, rng_key(seed, stream_id), k, workers, q_begin, q_end, base, d_out);
-    return cudaGetLastError();
+    const DrawGeom g = make_geom(n, wn, seed, stream_id, k, workers);
+    const uint64_t cnt = q_end - q_begin;
+    if (!ws || !use_region_plan(n, cnt)) {
+        const uint64_t span = static_cast<uint64_t>(K5_THREADS) * K5_UNROLL;
+        uint64_t blocks = (cnt + span - 1) / span;
+        const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8 * 64;
+        if (blocks > cap) blocks = cap;
+        k_sample<<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(d_b, g, q_begin, q_end, base,
+                                                                        d_out);
+        return cudaGetLastError();
+    }
+    const uint64_t chunk_max = region_chunk_max();
+    const uint64_t chunk = cnt < chunk_max ? cnt : chunk_max;
+    RegionPlan plan = plan_regions(g, chunk);
+    cudaError_t e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr));
+    if (e != cudaSuccess) return e;
+    RegionBuffers B;
+    region_bytes(plan, chunk, &B, ws->base);
+    ws->overflow = B.overflow;
+    const int sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg));
+    cudaFuncSetAttribute(k_region_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+    for (uint64_t c0 = q_begin; c0 < q_end; c0 += chunk) {
+        RegionGeom rg = plan.rg;
+        rg.q0 = c0;
+        rg.kc = (q_end - c0) < chunk ? (q_end - c0) : chunk;
+        rg.ntiles = (rg.kc + RS_TILE - 1) / RS_TILE;
+        e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st);
+        if (e != cudaSuccess) return e;
+        const unsigned tiles = static_cast<unsigned>(rg.ntiles);
+        k_region_scatter<<<tiles, RS_THREADS, sm_scatter, st>>>(rg, B.cursor, B.overflow, B.rec,
+                                                                B.slot_of, B.runs);
+        const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
+        k_region_gather<<<static_cast<unsigned>(gblocks), 256, 0, st>>>(rg, d_b, B.cursor, B.rec,
+                                                                        B.res);
+        k_region_unpermute<<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs, B.slot_of,
+                                                         B.res, base, d_out + (c0 - q_begin));
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_generate_uniform(double* d_w, uint64_t n, uint64_t offset, uint64_t seed,
