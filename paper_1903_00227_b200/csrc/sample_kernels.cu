@@ -103,9 +103,58 @@ struct KeyCache {
     }
 };
 
+// Walks a thread's increasing query positions: the current worker slice
+// [lo, hi) and its derived key.  W1 (a single worker, the common case)
+// compiles the slice logic away.
+template <bool W1>
+struct DrawCursor {
+    uint32_t w;
+    uint64_t lo, hi, key;
+    __device__ __forceinline__ void init(const DrawGeom& g, uint64_t q) {
+        if (W1) {
+            w = 0;
+            lo = 0;
+            hi = ~0ull;
+        } else {
+            uint64_t m;
+            locate(g, q, w, m);
+            lo = q - m;
+            hi = lo + g.per + (w < g.rem ? 1 : 0);
+        }
+        key = rng_derive(g.base_key, w);  // RngStream(seed, 'alia').derive(w), alias.hpp:279-280
+    }
+    // counter of output 2m+1 of query q (m = q - lo); q must not decrease
+    __device__ __forceinline__ uint64_t ctr1(const DrawGeom& g, uint64_t q) {
+        if (!W1) {
+            while (q >= hi) {
+                ++w;
+                lo = hi;
+                hi = lo + g.per + (w < g.rem ? 1 : 0);
+                key = rng_derive(g.base_key, w);
+            }
+        }
+        return key + (2 * (q - lo) + 1) * kGolden;
+    }
+};
+
 // bounded(n) of output 2m+1 (rng.hpp:63-66)
 __device__ __forceinline__ uint64_t draw_bucket(const DrawGeom& g, uint64_t key, uint64_t m) {
     return __umul64hi(mix64(key + (2 * m + 1) * kGolden), g.n);
+}
+// (r * n) >> 64 for n < 2^32 (the table limit) in two 32x32->64 multiplies;
+// equal to __umul64hi(r, n).
+__device__ __forceinline__ uint32_t mulhi_n32(uint64_t r, uint32_t n) {
+    const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(r)) * n;
+    const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(r >> 32)) * n + (t >> 32);
+    return static_cast<uint32_t>(u >> 32);
+}
+__device__ __forceinline__ uint64_t bucket_of_ctr(const DrawGeom& g, uint64_t c1) {
+    return mulhi_n32(mix64(c1), static_cast<uint32_t>(g.n));
+}
+// uniform01() * bucket_mean of the output after c1 (rng.hpp:53-55)
+__device__ __forceinline__ double coin_of_ctr(const DrawGeom& g, uint64_t c1) {
+    const uint64_t r = mix64(c1 + kGolden);
+    return (static_cast<double>(r >> 11) * 0x1.0p-53) * g.wn;
 }
 // uniform01() * bucket_mean of output 2m+2 (rng.hpp:53-55, alias.hpp:267)
 __device__ __forceinline__ double draw_coin(const DrawGeom& g, uint64_t key, uint64_t m) {
@@ -131,15 +180,17 @@ __device__ __forceinline__ uint32_t pick(const uint4& bk, double x) {
 constexpr int K5_THREADS = 256;
 constexpr int K5_UNROLL = 8;
 
+template <bool W1>
 __global__ void __launch_bounds__(K5_THREADS)
 k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_end,
          uint32_t out_base, uint32_t* __restrict__ out) {
     const uint64_t span = static_cast<uint64_t>(K5_THREADS) * K5_UNROLL;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * span;
     out -= q_begin;  // out[q] for q in [q_begin, q_end)
-    KeyCache kc;
-    for (uint64_t q0 = q_begin + static_cast<uint64_t>(blockIdx.x) * span + threadIdx.x;
-         q0 < q_end; q0 += stride) {
+    const uint64_t first = q_begin + static_cast<uint64_t>(blockIdx.x) * span + threadIdx.x;
+    DrawCursor<W1> cur;
+    cur.init(g, first < q_end ? first : q_begin);
+    for (uint64_t q0 = first; q0 < q_end; q0 += stride) {
         uint64_t bidx[K5_UNROLL];
         double x[K5_UNROLL];
 #pragma unroll
@@ -148,12 +199,9 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
             bidx[u] = 0;
             x[u] = 0.0;
             if (q < q_end) {
-                uint32_t w;
-                uint64_t m;
-                locate(g, q, w, m);
-                const uint64_t key = kc.get(g, w);
-                bidx[u] = draw_bucket(g, key, m);
-                x[u] = draw_coin(g, key, m);
+                const uint64_t c1 = cur.ctr1(g, q);
+                bidx[u] = bucket_of_ctr(g, c1);
+                x[u] = coin_of_ctr(g, c1);
             }
         }
         uint4 bk[K5_UNROLL];
@@ -166,7 +214,6 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
         }
     }
 }
-
 
 // ===========================================================================
 // region plan
@@ -249,6 +296,7 @@ __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg) {
     return ((head + 15) & ~size_t(15)) + RS_TILE * sizeof(uint2);
 }
 
+template <bool W1>
 __global__ void __launch_bounds__(RS_THREADS)
 k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restrict__ overflow,
                  uint2* __restrict__ rec, uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
@@ -263,19 +311,35 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     __syncthreads();
 
     uint32_t bk[RS_ROWS], rank[RS_ROWS];
-    KeyCache kc;
+    const uint32_t kc_left = static_cast<uint32_t>(umin64(rg.kc - tbase, RS_TILE));
+    const uint32_t n32 = static_cast<uint32_t>(rg.g.n);
+    if (W1) {
+        // single worker: counter of draw q is key + (2q + 1) G, and the rows of
+        // a thread are RS_THREADS draws apart
+        uint64_t c1 = rng_derive(rg.g.base_key, 0) +
+                      (2 * (rg.q0 + tbase + threadIdx.x) + 1) * kGolden;
+        const uint64_t step = 2ull * RS_THREADS * kGolden;
+#pragma unroll
+        for (int r = 0; r < RS_ROWS; ++r) {
+            bk[r] = mulhi_n32(mix64(c1), n32);
+            c1 += step;
+        }
+    } else {
+        DrawCursor<W1> cur;
+        cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
+#pragma unroll
+        for (int r = 0; r < RS_ROWS; ++r) {
+            const uint32_t e = r * RS_THREADS + threadIdx.x;
+            bk[r] = e < kc_left
+                        ? static_cast<uint32_t>(bucket_of_ctr(rg.g, cur.ctr1(rg.g, rg.q0 + tbase + e)))
+                        : 0u;
+        }
+    }
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
-        const uint64_t qc = tbase + r * RS_THREADS + threadIdx.x;
-        bk[r] = 0xffffffffu;
+        const uint32_t e = r * RS_THREADS + threadIdx.x;
         rank[r] = 0;
-        if (qc < rg.kc) {
-            uint32_t w;
-            uint64_t m;
-            locate(rg.g, rg.q0 + qc, w, m);
-            bk[r] = static_cast<uint32_t>(draw_bucket(rg.g, kc.get(rg.g, w), m));
-            rank[r] = atomicAdd(&loc[bk[r] >> rg.shift], 1u);
-        }
+        if (e < kc_left) rank[r] = atomicAdd(&loc[bk[r] >> rg.shift], 1u);
     }
     __syncthreads();
     if (warp == 0) {  // exclusive scan of the region counts, 32 at a time
@@ -295,13 +359,14 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
         if (lane == 0) loc[rg.nreg] = carry;
     }
     __syncthreads();
+    const uint32_t t32 = static_cast<uint32_t>(tbase);
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
-        const uint64_t qc = tbase + r * RS_THREADS + threadIdx.x;
-        if (qc < rg.kc) {
+        const uint32_t e = r * RS_THREADS + threadIdx.x;
+        if (e < kc_left) {
             const uint32_t slot = loc[bk[r] >> rg.shift] + rank[r];
-            stage[slot] = make_uint2(static_cast<uint32_t>(qc), bk[r]);
-            slot_of[qc] = static_cast<uint16_t>(slot);
+            stage[slot] = make_uint2(t32 + e, bk[r]);
+            slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
     }
     // claim slab space for each non-empty run of this tile
@@ -339,6 +404,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
 // contiguous run of 2048 slab positions per CTA, so the resident CTAs of the
 // GPU sweep the table region by region; table loads are marked evict-last,
 // record / result streams evict-first.
+template <bool W1>
 __global__ void __launch_bounds__(256)
 k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
                 const uint2* __restrict__ rec, uint32_t* __restrict__ res) {
@@ -350,6 +416,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     if (p0 >= valid_end) return;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
+    const uint64_t key0 = rng_derive(rg.g.base_key, 0);  // W1: the single worker's key
     uint2 r[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -363,10 +430,16 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     for (int u = 0; u < 8; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         if (p < valid_end) {
-            uint32_t w;
-            uint64_t m;
-            locate(rg.g, rg.q0 + r[u].x, w, m);
-            st_stream(res + p, pick(bk[u], draw_coin(rg.g, kc.get(rg.g, w), m)), pf);
+            double x;
+            if (W1) {
+                x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
+            } else {
+                uint32_t w;
+                uint64_t m;
+                locate(rg.g, rg.q0 + r[u].x, w, m);
+                x = draw_coin(rg.g, kc.get(rg.g, w), m);
+            }
+            st_stream(res + p, pick(bk[u], x), pf);
         }
     }
 }
@@ -376,6 +449,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 // then picks its answer at the slot RB recorded for it.  If a slab ever
 // overflowed (not expected: ~20 sigma of slack), the tile recomputes its
 // draws directly instead, so the output is correct in every case.
+template <bool W1>
 __global__ void __launch_bounds__(RS_THREADS)
 k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
                    const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
@@ -387,13 +461,11 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
     const uint64_t tbase = tile * RS_TILE;
     const uint32_t tcount = static_cast<uint32_t>(umin64(RS_TILE, rg.kc - tbase));
     if (*overflow) {
-        KeyCache kc;
+        DrawCursor<W1> cur;
+        cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
         for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS) {
-            uint32_t w;
-            uint64_t m;
-            locate(rg.g, rg.q0 + tbase + e, w, m);
-            const uint64_t key = kc.get(rg.g, w);
-            out[tbase + e] = pick(ld_bucket(b, draw_bucket(rg.g, key, m)), draw_coin(rg.g, key, m)) +
+            const uint64_t c1 = cur.ctr1(rg.g, rg.q0 + tbase + e);
+            out[tbase + e] = pick(ld_bucket(b, bucket_of_ctr(rg.g, c1)), coin_of_ctr(rg.g, c1)) +
                              out_base;
         }
         return;
@@ -530,8 +602,12 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
         uint64_t blocks = (cnt + span - 1) / span;
         const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8 * 64;
         if (blocks > cap) blocks = cap;
-        k_sample<<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(d_b, g, q_begin, q_end, base,
-                                                                        d_out);
+        if (g.W == 1)
+            k_sample<true><<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(d_b, g, q_begin,
+                                                                              q_end, base, d_out);
+        else
+            k_sample<false><<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(d_b, g, q_begin,
+                                                                               q_end, base, d_out);
         return cudaGetLastError();
     }
     const uint64_t chunk_max = region_chunk_max();
@@ -543,7 +619,11 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
     region_bytes(plan, chunk, &B, ws->base);
     ws->overflow = B.overflow;
     const int sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg));
-    cudaFuncSetAttribute(k_region_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+    const bool w1 = g.W == 1;
+    cudaFuncSetAttribute(k_region_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sm_scatter);
+    cudaFuncSetAttribute(k_region_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sm_scatter);
     for (uint64_t c0 = q_begin; c0 < q_end; c0 += chunk) {
         RegionGeom rg = plan.rg;
         rg.q0 = c0;
@@ -552,13 +632,23 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
         e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st);
         if (e != cudaSuccess) return e;
         const unsigned tiles = static_cast<unsigned>(rg.ntiles);
-        k_region_scatter<<<tiles, RS_THREADS, sm_scatter, st>>>(rg, B.cursor, B.overflow, B.rec,
-                                                                B.slot_of, B.runs);
         const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
-        k_region_gather<<<static_cast<unsigned>(gblocks), 256, 0, st>>>(rg, d_b, B.cursor, B.rec,
-                                                                        B.res);
-        k_region_unpermute<<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs, B.slot_of,
-                                                         B.res, base, d_out + (c0 - q_begin));
+        uint32_t* o = d_out + (c0 - q_begin);
+        if (w1) {
+            k_region_scatter<true><<<tiles, RS_THREADS, sm_scatter, st>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+            k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
+                rg, d_b, B.cursor, B.rec, B.res);
+            k_region_unpermute<true><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,
+                                                                   B.slot_of, B.res, base, o);
+        } else {
+            k_region_scatter<false><<<tiles, RS_THREADS, sm_scatter, st>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+            k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
+                rg, d_b, B.cursor, B.rec, B.res);
+            k_region_unpermute<false><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,
+                                                                    B.slot_of, B.res, base, o);
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwrs_b200.so")
+# WRS_B200_LIB selects another build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("WRS_B200_LIB") or os.path.join(HERE, "libwrs_b200.so")
 
 WRS_OK, WRS_EINVAL, WRS_EIO, WRS_EFORMAT, WRS_EVERIFY, WRS_ENOMEM, WRS_EINTERNAL = range(7)
 KEEP_WORKSPACE = 1
