@@ -47,8 +47,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_ITEMS, help="items per GPU")
-    ap.add_argument("--k", type=int, default=K_SAMPLES, help="draws per GPU")
+    ap.add_argument("--items", dest="n", type=int, default=N_ITEMS, help="items per GPU")
+    ap.add_argument("--draws", dest="k", type=int, default=K_SAMPLES, help="draws per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -218,21 +218,32 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("WRS_BENCH_BACKEND", "nccl")  # gloo: 1-GPU smoke of the N>1 path
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
 
     n_total, k_total = args.n * world, args.k * world
     lo, hi = wrs.shard_range(n_total, world, rank)
     W = wrs.Weights.generate_range("uniform", 0.0, n_total, lo, hi, SEED)
-    S = wrs.Sampler.build(W, "psa", 1)
     n_local = hi - lo
-    out = torch.empty(int(args.k * 1.2) + 1024 if world > 1 else args.k, dtype=torch.int32,
-                      device=dev)
-    tot = torch.zeros(world, dtype=torch.float64, device=dev)
-    mine = torch.tensor([W.total()], dtype=torch.float64, device=dev)
+    if world > 1:
+        from paper_1903_00227_b200.sharded import ShardedSampler
+        shard = ShardedSampler(W, n_total, rank, world)
+        S = shard.sampler
+        cap = int(shard.counts(SEED, k_total).max()) + 1024
+    else:
+        shard = None
+        S = wrs.Sampler.build(W, "psa", 1)
+        cap = args.k
+    out = torch.empty(cap, dtype=torch.int32, device=dev)
 
     def step(ev=None):
         with torch.cuda.stream(stream):
@@ -241,17 +252,21 @@ def main():
             S.rebuild_async(stream)
             if ev:
                 ev[1].record(stream)
-            if world > 1:
-                dist.all_gather_into_tensor(tot, mine)
-                counts = wrs.shard_counts(tot.cpu().numpy(), SEED, k_total)
-                k_me = int(counts[rank])
-                S.draw_shard_device(SEED, rank, k_me, lo, out, stream)
+            if shard is not None:
+                # the shard totals come with the weights (K0 at creation); a
+                # fresh job re-gathers them: one collective of G doubles
+                shard.totals = shard_gather(W.total())
+                k_me = shard.draw_device(SEED, k_total, out, stream)
             else:
                 k_me = args.k
                 S.draw_device(SEED, k_me, 1, out, stream)
             if ev:
                 ev[2].record(stream)
         return k_me
+
+    def shard_gather(t):
+        from paper_1903_00227_b200.sharded import default_gather
+        return default_gather(t)
 
     for _ in range(args.warmup):
         step()
@@ -285,8 +300,9 @@ def main():
     build_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     draw_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     ms_step = ms / args.steps
-    if world > 1:
-        m = torch.tensor([ms_step, build_ms, draw_ms], dtype=torch.float64, device=dev)
+    if world > 1:  # max over ranks
+        mdev = dev if backend == "nccl" else torch.device("cpu")
+        m = torch.tensor([ms_step, build_ms, draw_ms], dtype=torch.float64, device=mdev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         ms_step, build_ms, draw_ms = m.tolist()
 
@@ -376,7 +392,8 @@ def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):
     sec = statistics.median(times)
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        tdev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([sec], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
     return {"value": (n_total + k * world) / sec / 1e9, "unit": UNIT,

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("WRS_B200_LIB") or os.path.join(HERE, "libwrs_b200.so"
 
 WRS_OK, WRS_EINVAL, WRS_EIO, WRS_EFORMAT, WRS_EVERIFY, WRS_ENOMEM, WRS_EINTERNAL = range(7)
 KEEP_WORKSPACE = 1
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 BUCKET_DTYPE = np.dtype([("share", "<f8"), ("item", "<u4"), ("alias", "<u4")])
 
@@ -123,10 +124,19 @@ def _dev_ptr(t) -> int:
     return t if isinstance(t, int) else t.data_ptr()
 
 
-def _stream_ptr(stream) -> int | None:
+def _stream_ptr(stream, out=None) -> int | None:
+    """cudaStream_t for a call.  With no explicit stream and a torch tensor as
+    the output, the tensor's current torch stream is used, so the library's
+    writes are ordered with torch's own use (and reuse) of that memory."""
     if stream is None:
-        return None
-    return stream if isinstance(stream, int) else stream.cuda_stream
+        if out is None or not hasattr(out, "device"):
+            return None  # the handle's own stream
+        import torch
+        stream = torch.cuda.current_stream(out.device)
+    h = stream if isinstance(stream, int) else stream.cuda_stream
+    # torch's default stream is the legacy stream (handle 0); NULL means "the
+    # handle's own stream" to the ABI, so name the legacy stream explicitly
+    return h if h else CUDA_STREAM_LEGACY
 
 
 def default_jobs(n: int) -> int:
@@ -275,12 +285,12 @@ class Sampler:
 
     def draw_device(self, seed: int, count: int, workers: int, out, stream=None) -> None:
         _check(lib().wrs_b200_sampler_draw_device(self.h, seed, count, workers,
-                                                  _dev_ptr(out), _stream_ptr(stream)))
+                                                  _dev_ptr(out), _stream_ptr(stream, out)))
 
     def draw_shard_device(self, seed: int, shard: int, count: int, base: int, out,
                           stream=None) -> None:
         _check(lib().wrs_b200_sampler_draw_shard_device(self.h, seed, shard, count, base,
-                                                        _dev_ptr(out), _stream_ptr(stream)))
+                                                        _dev_ptr(out), _stream_ptr(stream, out)))
 
     def stage(self, name: str) -> np.ndarray:
         dtypes = {"counts": np.uint64, "heavy": np.uint32, "light_alias": np.uint32,
