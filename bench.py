@@ -37,8 +37,8 @@ UNIT = "G(items+samples)/s"
 BUILD_BYTES_PER_ITEM = 72   # SURVEY.md §8(d) minus K0 (W comes with the weights, as the
                             # reference's WeightTable): K1 20 + K2 24 + K4 28
 SAMPLE_BYTES_PER_DRAW = 36  # one 32-B sector gather + one 4-B index store
-KERNELS_PER_STEP = 8        # k_partition, k_scan_blocks x2, k_scan_carry, k_split,
-                            # k_pack, k_assemble, k_sample
+KERNELS_PER_STEP = 10       # build: k_partition, k_scan_blocks x2, k_scan_carry, k_split,
+                            # k_pack, k_assemble; draw: k_region_scatter, _gather, _unpermute
 
 
 def parse():
@@ -126,6 +126,19 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
+def host_cpu() -> str:
+    model, sockets = "unknown", set()
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name") and model == "unknown":
+                model = line.split(":", 1)[1].strip()
+            if line.startswith("physical id"):
+                sockets.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return f"{model}, {os.cpu_count()} hw threads, {max(1, len(sockets))} socket(s)"
+
+
 # ------------------------------------------------------------- CPU arm
 def cpu_reference_step(n: int, k: int, k_sample: int, threads: int, w=None):
     """One bounded sample of the workload on the host: the reference's
@@ -193,7 +206,7 @@ def run_reference(args):
         "config": {"workload": "BASELINE configs[1]: n=1e8 uniform(0,1] f64, psa build + 1e9 draws",
                    "n": n, "k": k},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": detail["cores"],
-                         "kind": detail["kind"],
+                         "kind": detail["kind"], "host": host_cpu(),
                          "sample": f"AliasTable(wt, psa, {threads}) over n={n} (median of "
                                    f"{args.steps}) + sample_many({threads} threads) over "
                                    f"{k_sample} draws extrapolated to k={k}",
@@ -330,15 +343,17 @@ def main():
         "build": {"gitems_per_s": n_local / (build_ms * 1e-3) / 1e9, "ms": build_ms,
                   "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": hbm,
                                "peak_kind": hbm_kind, "unit": "GB/s", "frac": build_gbs / hbm,
-                               "bytes_per_item": BUILD_BYTES_PER_ITEM},
+                               "bytes_per_item": BUILD_BYTES_PER_ITEM,
+                               "traffic": traffic("build_bytes_per_item", n_local)},
                   "stages_ms": dict(zip(["K1_partition", "K2a_block_totals", "K2b_carries",
                                          "K2c_prefixes", "K3_splits", "K4a_pack", "K4b_assemble"],
                                         [round(x, 4) for x in stage_ms]))},
         "sample": {"gsamples_per_s": k_per_rank / (draw_ms * 1e-3) / 1e9, "ms": draw_ms},
-        "roofline": {"bound": "hbm", "kernel": "k_sample", "achieved": draw_gbs, "peak": hbm,
-                     "peak_kind": hbm_kind, "unit": "GB/s", "frac": draw_gbs / hbm,
-                     "bytes_per_sample": SAMPLE_BYTES_PER_DRAW,
-                     "traffic": traffic("k_sample_bytes_per_sample", k_per_rank)},
+        "roofline": {"bound": "hbm",
+                     "kernel": "draw stage: k_region_scatter + k_region_gather + k_region_unpermute",
+                     "achieved": draw_gbs, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
+                     "frac": draw_gbs / hbm, "bytes_per_sample": SAMPLE_BYTES_PER_DRAW,
+                     "traffic": traffic("draw_bytes_per_sample", k_per_rank)},
         "gpu_launches": KERNELS_PER_STEP * args.steps,
         "clocks": clocks.summary(),
     }
@@ -352,7 +367,7 @@ def main():
         t, d = cpu_reference_step(args.n, args.k, min(args.k, 10**8), os.cpu_count() or 1)
         result["cpu_baseline"] = {
             "value": (args.n + args.k) / t / 1e9, "unit": UNIT, "cores": d["cores"],
-            "kind": d["kind"],
+            "kind": d["kind"], "host": host_cpu(),
             "sample": f"AliasTable(wt, psa, {d['cores']}) over n={args.n} + sample_many over "
                       f"1e8 draws extrapolated to k={args.k}",
             "build_s": d["build_s"], "draw_s_per_1e9": d["draw_s_per_1e9"]}
