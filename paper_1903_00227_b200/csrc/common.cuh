@@ -61,7 +61,11 @@ struct CompSum {
     double hi, lo;
     __device__ __forceinline__ void add(double x) {
         const double t = hi + x;
-        const double e = fabs(hi) >= fabs(x) ? (hi - t) + x : (x - t) + hi;
+        // (hi - t) + x if |hi| >= |x| else (x - t) + hi: select the operands,
+        // then the same two roundings (2 DADD instead of 4 + a select)
+        const bool big = fabs(hi) >= fabs(x);
+        const double a = big ? hi : x, b = big ? x : hi;
+        const double e = (a - t) + b;
         const double l2 = lo + e;
         lo = isfinite(t) ? l2 : lo;
         hi = t;
@@ -81,6 +85,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>

@@ -622,6 +622,20 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
         cp_async_wait<0>();
         __syncwarp();
 
+        // Prefetch into L2 the lines the next phase's windows most likely
+        // need ([i+S, i+2S) and the heavy run after this window), so the next
+        // staging copies hit L2 instead of HBM.
+        if (live) {
+            const char* pl = reinterpret_cast<const char*>(lw + umin64(wl0 + K4_S, lhi));
+            const char* ph = reinterpret_cast<const char*>(hw + umin64(wh0 + K4_S, nh - 1));
+            const char* pi = reinterpret_cast<const char*>(hidx + umin64(wh0 + K4_S, nh - 1));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pl));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pl + 128));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ph));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ph + 128));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pi));
+        }
+
         // ---- up to K4_S sequential steps per lane ---------------------------
         // Branch-free: every lane evaluates the same instruction stream, the
         // operation (light bucket / heavy bucket / none) is a predicate.
@@ -714,42 +728,51 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
            const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lalias,
            const double* __restrict__ hshare, const uint32_t* __restrict__ halias,
            Bucket* __restrict__ out) {
+    // The tile's lights are the contiguous light-list run [L0, L0 + totL) and
+    // its heavies the run [H0, H0 + totH): both runs are staged into shared
+    // memory with coalesced async copies, then every item reads its alias /
+    // share from there (no dependent global gathers).
+    extern __shared__ __align__(16) unsigned char k4b_smem[];
     __shared__ TileCells C;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t tile = blockIdx.x;
     const uint64_t base = tile * K1_TILE;
     const bool uniform = sc->nh == 0;
     classify_tile<false>(w, n, base, sc->wn, nullptr, C);
-    const uint64_t L0 = (status[tile] & VAL_MASK) - C.totL;
+    const uint32_t totL = C.totL, totH = C.totH;
+    const uint64_t L0 = (status[tile] & VAL_MASK) - totL;
     const uint64_t H0 = base - L0;
+    uint32_t* s_la = reinterpret_cast<uint32_t*>(k4b_smem);
+    double* s_hs = reinterpret_cast<double*>(k4b_smem + ((4u * totL + 15u) & ~15u));
+    uint32_t* s_ha = reinterpret_cast<uint32_t*>(s_hs + totH);
+    if (!uniform) {
+        for (uint32_t i = threadIdx.x; i < totL; i += K1_THREADS) cp_async4(&s_la[i], lalias + L0 + i);
+        for (uint32_t i = threadIdx.x; i < totH; i += K1_THREADS) {
+            cp_async8(&s_hs[i], hshare + H0 + i);
+            cp_async4(&s_ha[i], halias + H0 + i);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    }
+    __syncthreads();
     const unsigned lt = lanemask_lt();
-    // Two half-tiles: issue all loads of 8 rows, then their 8 stores, so each
-    // thread has 8 independent gathers in flight.
-#pragma unroll
-    for (int h = 0; h < K1_ROWS; h += 8) {
-        double share[8];
-        uint32_t alias[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int r = h + u;
-            const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
-            const int cell = r * 8 + warp;
-            const unsigned lm = C.lm[cell];
-            const bool light = (lm >> lane) & 1;
-            const uint64_t p = light ? L0 + C.exL[cell] + __popc(lm & lt)
-                                     : H0 + C.exH[cell] + __popc(C.hm[cell] & lt);
-            share[u] = 0.0;
-            alias[u] = static_cast<uint32_t>(gi);
-            if (gi < n) {
-                share[u] = light ? __ldg(w + gi) : __ldg(hshare + p);
-                if (!uniform) alias[u] = light ? __ldg(lalias + p) : __ldg(halias + p);
-            }
+#pragma unroll 4
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
+        if (gi >= n) continue;
+        const int cell = r * 8 + warp;
+        const unsigned lm = C.lm[cell];
+        double share;
+        uint32_t alias = static_cast<uint32_t>(gi);
+        if ((lm >> lane) & 1) {
+            share = __ldg(w + gi);
+            if (!uniform) alias = s_la[C.exL[cell] + __popc(lm & lt)];
+        } else {
+            const uint32_t p = C.exH[cell] + __popc(C.hm[cell] & lt);
+            share = s_hs[p];
+            alias = s_ha[p];
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const uint64_t gi = base + (h + u) * K1_THREADS + threadIdx.x;
-            if (gi < n) store_bucket(out, gi, share[u], static_cast<uint32_t>(gi), alias[u]);
-        }
+        store_bucket(out, gi, share, static_cast<uint32_t>(gi), alias);
     }
 }
 
@@ -869,6 +892,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     // per-device attribute; cheap enough to set on every build
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
     cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
+    cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, K1_TILE * 12 + 16);
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
     const unsigned k2_grid = static_cast<unsigned>((nblocks + K2_WARPS * 32 - 1) / (K2_WARPS * 32));
@@ -903,7 +927,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
                                                     ws.split_h, ws.split_s, ws.lalias, ws.hshare,
                                                     ws.halias);
     REC(6);
-    k_assemble<<<static_cast<unsigned>(ntiles), K1_THREADS, 0, st>>>(
+    k_assemble<<<static_cast<unsigned>(ntiles), K1_THREADS, K1_TILE * 12 + 16, st>>>(
         d_w, n, ws.sc, ws.tile_status, ws.lalias, ws.hshare, ws.halias, d_b);
     REC(7);
 #undef REC

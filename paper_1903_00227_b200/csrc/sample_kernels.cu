@@ -217,8 +217,8 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
 
 // ===========================================================================
 // region plan
-//   Tiles of RS_TILE consecutive draws; warp w of a tile owns the RS_SUB
-//   consecutive draws [w*RS_SUB, (w+1)*RS_SUB) in rows of 32.  Inside a tile
+//   Tiles of RS_TILE consecutive draws; warp w of a tile owns the RS_ROWS*32
+//   consecutive draws starting at w*RS_ROWS*32, in rows of 32.  Inside a tile
 //   the draws are laid out by (region, warp, row, lane); each region's run of
 //   the tile moves to and from global memory as one contiguous block through
 //   shared memory.  Region r owns a fixed slab [r*cap, (r+1)*cap) of the
@@ -231,7 +231,6 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ROWS = 16;                        // rows of 32 draws per warp
 constexpr int RS_TILE = RS_THREADS * RS_ROWS;      // 4096 draws per tile
-constexpr int RS_SUB = 32 * RS_ROWS;               // 512 consecutive draws per warp
 constexpr int RS_MAX_REGIONS = 1024;
 
 struct RegionGeom {
@@ -364,7 +363,8 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     for (int r = 0; r < RS_ROWS; ++r) {
         const uint32_t e = r * RS_THREADS + threadIdx.x;
         if (e < kc_left) {
-            const uint32_t slot = loc[bk[r] >> rg.shift] + rank[r];
+            const uint32_t reg = bk[r] >> rg.shift;
+            const uint32_t slot = loc[reg] + rank[r];
             stage[slot] = make_uint2(t32 + e, bk[r]);
             slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
@@ -388,6 +388,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     }
     __syncthreads();
     if (*overflow) return;
+    // each region's run of the staged tile -> one contiguous slab block
     const uint64_t pol = policy_evict_first();
     for (uint32_t reg = warp; reg < rg.nreg; reg += RS_WARPS) {  // one run per warp
         const uint32_t l0 = loc[reg], c = loc[reg + 1] - l0;
