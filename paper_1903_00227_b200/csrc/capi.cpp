@@ -92,6 +92,13 @@ struct DevBuf {
 struct Stream {
     cudaStream_t s = nullptr;
     Stream() { ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate"); }
+    // prio > 0: the device's greatest priority, prio < 0: its least
+    explicit Stream(int prio) {
+        int least = 0, greatest = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+        ck(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio > 0 ? greatest : least),
+           "cudaStreamCreate");
+    }
     ~Stream() {
         if (s) cudaStreamDestroy(s);
     }
@@ -209,11 +216,24 @@ struct wrs_sampler {
     mutable wrsb::SampleWorkspace sws;
     mutable std::mutex sws_mu;
     mutable cudaEvent_t sws_ev = nullptr;
+    // side stream for the table-independent first stage of a draw (the
+    // region scatter), so it overlaps a rebuild queued before the draw
+    mutable std::unique_ptr<Stream> side;
+    mutable cudaEvent_t side_ev = nullptr;
+    // rebuilds run on a high-priority stream (event handoff from / to the
+    // caller's stream) so their CTAs win the SMs over a concurrent scatter
+    std::unique_ptr<Stream> hi;
+    cudaEvent_t hi_ev[2] = {};
 
     ~wrs_sampler() {
         if (device >= 0) cudaSetDevice(device);
         wrsb::workspace_free(ws);
         if (sws_ev) cudaEventSynchronize(sws_ev), cudaEventDestroy(sws_ev);
+        if (side_ev) cudaEventSynchronize(side_ev), cudaEventDestroy(side_ev);
+        side.reset();
+        for (cudaEvent_t& e : hi_ev)
+            if (e) cudaEventSynchronize(e), cudaEventDestroy(e);
+        hi.reset();
         sws.release();
         for (cudaEvent_t& e : ev)
             if (e) cudaEventDestroy(e);
@@ -262,10 +282,15 @@ std::unique_ptr<wrs_sampler> build_psa(const std::shared_ptr<WeightsData>& wd, u
 void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, uint64_t k,
                uint32_t workers, uint32_t base, uint32_t* out, cudaStream_t st) {
     std::lock_guard<std::mutex> g(s.sws_mu);
-    if (!s.sws_ev) ck(cudaEventCreateWithFlags(&s.sws_ev, cudaEventDisableTiming), "event");
+    if (!s.sws_ev) {
+        ck(cudaEventCreateWithFlags(&s.sws_ev, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&s.side_ev, cudaEventDisableTiming), "event");
+        s.side = std::make_unique<Stream>();
+    }
     ck(cudaStreamWaitEvent(st, s.sws_ev, 0), "wait");
+    ck(cudaStreamWaitEvent(s.side->s, s.sws_ev, 0), "wait");
     ck(wrsb::launch_sample(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, q0, q1, k, workers, base,
-                           out, st, &s.sws),
+                           out, st, &s.sws, s.side->s, s.side_ev),
        "K5 launch");
     ck(cudaEventRecord(s.sws_ev, st), "event");
 }
@@ -640,9 +665,18 @@ wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream) {
         s->timed = g_timing.load() != 0;
         if (s->timed && !s->ev[0])
             for (cudaEvent_t& e : s->ev) ck(cudaEventCreate(&e), "event");
+        if (!s->hi) {
+            s->hi = std::make_unique<Stream>(1);
+            for (cudaEvent_t& e : s->hi_ev)
+                ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        }
+        ck(cudaEventRecord(s->hi_ev[0], st), "event");
+        ck(cudaStreamWaitEvent(s->hi->s, s->hi_ev[0], 0), "wait");
         ck(wrsb::launch_psa_build(s->weights->d_w, s->n, s->weights->total, s->P, s->d_b(),
-                                  s->ws, st, s->timed ? s->ev : nullptr),
+                                  s->ws, s->hi->s, s->timed ? s->ev : nullptr),
            "PSA launch");
+        ck(cudaEventRecord(s->hi_ev[1], s->hi->s), "event");
+        ck(cudaStreamWaitEvent(st, s->hi_ev[1], 0), "wait");
         return WRS_OK;
     });
 }

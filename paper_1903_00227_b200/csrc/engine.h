@@ -78,11 +78,17 @@ struct SampleWorkspace {
 // `stream_id` is the reference's sample stream 0x616c6961 ("alia").  `base` is
 // added to every output (global ids of a shard).  With a workspace, large
 // tables use the region-ordered plan; without, the direct gather kernel.
+// `side` (optional): a stream on which the region plan's first scatter runs.
+// The scatter reads nothing but (n, seed, k), so it need not wait for the
+// table: it only waits for what `side` already carries (the previous user of
+// the scratch), and st waits for it (side_ev) before the first gather.  A
+// draw issued right behind a rebuild thus scatters while the build runs.
 constexpr uint64_t kSampleStream = 0x616c6961u;
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
                           uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,
-                          SampleWorkspace* ws);
+                          SampleWorkspace* ws, cudaStream_t side = nullptr,
+                          cudaEvent_t side_ev = nullptr);
 bool use_region_plan(uint64_t n, uint64_t k);
 
 // generate_uniform on the device (weight_file.hpp:32-38): counter-based, so

@@ -292,7 +292,7 @@ __device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t 
 // never needs to be reproduced.
 __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg) {
     const size_t head = (2 * static_cast<size_t>(nreg) + 1) * 4;
-    return ((head + 15) & ~size_t(15)) + RS_TILE * sizeof(uint2);
+    return ((head + 15) & ~size_t(15)) + RS_TILE * sizeof(uint2) + RS_TILE * sizeof(uint16_t);
 }
 
 template <bool W1>
@@ -303,6 +303,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     uint32_t* loc = reinterpret_cast<uint32_t*>(rs_smem);  // counts, then run starts
     uint32_t* goff = loc + rg.nreg + 1;
     uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((2 * rg.nreg + 1) * 4 + 15) & ~15u));
+    uint16_t* regmap = reinterpret_cast<uint16_t*>(stage + RS_TILE);  // region of each staged slot
     const uint64_t tile = blockIdx.x;
     const uint64_t tbase = tile * RS_TILE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -366,6 +367,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
             const uint32_t reg = bk[r] >> rg.shift;
             const uint32_t slot = loc[reg] + rank[r];
             stage[slot] = make_uint2(t32 + e, bk[r]);
+            regmap[slot] = static_cast<uint16_t>(reg);
             slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
     }
@@ -383,20 +385,25 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
                 g = rg.nreg * rg.cap + (ob + c <= rg.ov_cap ? ob : 0);
             }
         }
-        goff[reg] = g;
+        goff[reg] = g - loc[reg];  // slab position of staged slot i = goff[region] + i
         runs[tile * rg.nreg + reg] = RunInfo{g, loc[reg]};
     }
     __syncthreads();
-    if (*overflow) return;
-    // each region's run of the staged tile -> one contiguous slab block
+    // (no early exit on overflow: an overflowed run is written to the start
+    // of the overflow slab, which stays in bounds, and RD recomputes the whole
+    // chunk directly whenever the flag is set)
+    // staged tile -> slabs: slot i goes to goff[regmap[i]] + i, so consecutive
+    // slots of a run land on consecutive slab positions (one flat, fully
+    // unrolled pass; no per-run loop)
     const uint64_t pol = policy_evict_first();
-    for (uint32_t reg = warp; reg < rg.nreg; reg += RS_WARPS) {  // one run per warp
-        const uint32_t l0 = loc[reg], c = loc[reg + 1] - l0;
-        uint2* dst = rec + goff[reg];
-        for (uint32_t t = lane; t < c; t += 32) {
-            const uint2 v = stage[l0 + t];
+#pragma unroll
+    for (int r = 0; r < RS_ROWS; ++r) {
+        const uint32_t i = r * RS_THREADS + threadIdx.x;
+        if (i < kc_left) {
+            const uint2 v = stage[i];
+            uint2* dst = rec + (goff[regmap[i]] + i);
             asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
-                         :: "l"(dst + t), "r"(v.x), "r"(v.y), "l"(pol));
+                         :: "l"(dst), "r"(v.x), "r"(v.y), "l"(pol));
         }
     }
 }
@@ -424,12 +431,22 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
     }
-    uint4 bk[8];
+    // bucket gathers as LDGSTS into shared memory: measured 232 G random
+    // L2-resident 16-B rows/s vs 200 G for LDG (scripts/microbench/
+    // l2_gather_bench.cu); each thread reads back only its own rows
+    __shared__ uint4 bk_s[8 * 256];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) bk[u] = ld_table(b, r[u].y, pl);
+    for (int u = 0; u < 8; ++u) {
+        const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
+                     ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
+        const uint4 bk = bk_s[u * 256 + threadIdx.x];
         if (p < valid_end) {
             double x;
             if (W1) {
@@ -440,7 +457,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
                 locate(rg.g, rg.q0 + r[u].x, w, m);
                 x = draw_coin(rg.g, kc.get(rg.g, w), m);
             }
-            st_stream(res + p, pick(bk[u], x), pf);
+            st_stream(res + p, pick(bk, x), pf);
         }
     }
 }
@@ -471,17 +488,43 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         }
         return;
     }
-    const uint64_t pf = policy_evict_first();
     const RunInfo* tr = runs + tile * rg.nreg;
+    // full tiles with a 16-B aligned output: each thread owns 4 consecutive
+    // draws per pass (one 8-B slot vector, one 16-B output store); the slot
+    // vectors are loaded first so they are in flight during the staging
+    constexpr int VP = RS_TILE / (RS_THREADS * 4);  // passes of 4 draws
+    const bool vec = tcount == RS_TILE && (reinterpret_cast<uintptr_t>(out + tbase) & 15) == 0;
+    uint2 sv[VP];
+    if (vec) {
+#pragma unroll
+        for (int i = 0; i < VP; ++i)
+            sv[i] = *reinterpret_cast<const uint2*>(slot_of + tbase + (i * RS_THREADS + threadIdx.x) * 4);
+    }
+    // this tile's runs -> shared memory with LDGSTS: no register staging, so
+    // every element of the tile is in flight at once
     for (uint32_t reg = warp; reg < rg.nreg; reg += RS_WARPS) {
         const RunInfo ri = tr[reg];
         const uint32_t l1 = reg + 1 < rg.nreg ? tr[reg + 1].loc : tcount;
-        for (uint32_t t = lane; t < l1 - ri.loc; t += 32)
-            stage[ri.loc + t] = ld_stream(res + ri.goff + t, pf);
+        for (uint32_t t = lane; t < l1 - ri.loc; t += 32) cp_async4(&stage[ri.loc + t], res + ri.goff + t);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS)
-        out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
+    if (vec) {
+#pragma unroll
+        for (int i = 0; i < VP; ++i) {
+            const uint32_t e0 = (i * RS_THREADS + threadIdx.x) * 4;
+            uint4 o;
+            o.x = stage[sv[i].x & 0xffffu] + out_base;
+            o.y = stage[sv[i].x >> 16] + out_base;
+            o.z = stage[sv[i].y & 0xffffu] + out_base;
+            o.w = stage[sv[i].y >> 16] + out_base;
+            *reinterpret_cast<uint4*>(out + tbase + e0) = o;
+        }
+    } else {
+        for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS)
+            out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
+    }
 }
 
 // ===========================================================================
@@ -594,7 +637,7 @@ void SampleWorkspace::release() {
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
                           uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,
-                          SampleWorkspace* ws) {
+                          SampleWorkspace* ws, cudaStream_t side, cudaEvent_t side_ev) {
     if (q_end <= q_begin) return cudaSuccess;
     const DrawGeom g = make_geom(n, wn, seed, stream_id, k, workers);
     const uint64_t cnt = q_end - q_begin;
@@ -630,21 +673,31 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
         rg.q0 = c0;
         rg.kc = (q_end - c0) < chunk ? (q_end - c0) : chunk;
         rg.ntiles = (rg.kc + RS_TILE - 1) / RS_TILE;
-        e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st);
+        // first chunk's scatter on the side stream (if any): it does not read
+        // the table; later chunks reuse the scratch behind RD on st
+        const bool on_side = side && side_ev && c0 == q_begin;
+        cudaStream_t ss = on_side ? side : st;
+        e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, ss);
         if (e != cudaSuccess) return e;
         const unsigned tiles = static_cast<unsigned>(rg.ntiles);
         const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
         uint32_t* o = d_out + (c0 - q_begin);
-        if (w1) {
-            k_region_scatter<true><<<tiles, RS_THREADS, sm_scatter, st>>>(
+        if (w1)
+            k_region_scatter<true><<<tiles, RS_THREADS, sm_scatter, ss>>>(
                 rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+        else
+            k_region_scatter<false><<<tiles, RS_THREADS, sm_scatter, ss>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+        if (on_side) {
+            if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
+        }
+        if (w1) {
             k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
                 rg, d_b, B.cursor, B.rec, B.res);
             k_region_unpermute<true><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,
                                                                    B.slot_of, B.res, base, o);
         } else {
-            k_region_scatter<false><<<tiles, RS_THREADS, sm_scatter, st>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
             k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
                 rg, d_b, B.cursor, B.rec, B.res);
             k_region_unpermute<false><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,
