@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--draws", dest="k", type=int, default=K_SAMPLES, help="draws per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-aggregate", action="store_true")
     return ap.parse_args()
 
 
@@ -374,6 +375,11 @@ def main():
         "clocks": clocks.summary(),
     }
 
+    # ---- aggregated draws (BASELINE configs[3] shape, on this GPU) ------------
+    if world == 1 and not args.no_aggregate:
+        del out
+        result["aggregate"] = aggregate(args, wrs, torch, dev, stream)
+
     # ---- end to end through the C ABI with host buffers ---------------------
     if not args.no_e2e:
         result["e2e"] = e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total)
@@ -392,6 +398,39 @@ def main():
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result))
+
+
+def aggregate(args, wrs, torch, dev, stream):
+    """BASELINE configs[3] on one GPU: n lognormal(0, 2) weights, k draws
+    aggregated to (item, count) pairs (wrs_b200_sampler_draw_counts_device):
+    the same alias draws as the main line, counted instead of written."""
+    n, k = args.n, args.k
+    g = torch.Generator(device=dev).manual_seed(SEED)
+    wt = torch.exp(2.0 * torch.randn(n, dtype=torch.float64, device=dev, generator=g))
+    W = wrs.Weights.from_device(wt)
+    S = wrs.Sampler.build(W, "psa", 1)
+    cap = min(n, k)
+    items = torch.empty(cap, dtype=torch.int32, device=dev)
+    counts = torch.empty(cap, dtype=torch.int64, device=dev)
+    m = torch.zeros(1, dtype=torch.int64, device=dev)
+    for _ in range(2):
+        S.draw_counts_device(SEED, k, 1, items, counts, m, stream)
+    torch.cuda.synchronize()
+    reps = max(args.steps, 3)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        S.draw_counts_device(SEED, k, 1, items, counts, m, stream)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    nu = int(m.item())
+    assert int(counts[:nu].sum()) == k
+    return {"workload": "BASELINE configs[3] on 1 GPU: n=%d lognormal(0,2) f64 weights "
+                        "(torch cuda generator, seed %d), k=%d draws -> (item, count) pairs"
+                        % (n, SEED, k),
+            "gsamples_per_s": k / (ms * 1e-3) / 1e9, "ms": ms, "n_unique": nu,
+            "gpu_launches": 7}
 
 
 def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):

@@ -66,6 +66,20 @@ WRS_API wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t s
                                                 uint64_t count, unsigned workers,
                                                 uint32_t* d_out, void* stream);
 
+/* Aggregated draws: the distinct items of
+ * wrs_sampler_draw(s, seed, k, workers, ...) with their multiplicities,
+ * items ascending.  items / counts hold min(k, n) entries; *n_unique gets
+ * the number written; the counts sum to k.  The draws are the same as the
+ * plain draw's, so the pairs are exactly the histogram of that output.
+ * _device: device outputs (n_unique too), asynchronous on `stream`. */
+WRS_API wrs_status wrs_b200_sampler_draw_counts(const wrs_sampler* s, uint64_t seed, uint64_t k,
+                                                unsigned workers, uint32_t* items,
+                                                uint64_t* counts, uint64_t* n_unique);
+WRS_API wrs_status wrs_b200_sampler_draw_counts_device(const wrs_sampler* s, uint64_t seed,
+                                                       uint64_t k, unsigned workers,
+                                                       uint32_t* d_items, uint64_t* d_counts,
+                                                       uint64_t* d_n_unique, void* stream);
+
 /* Copy a named intermediate of the last build (needs WRS_B200_KEEP_WORKSPACE):
  * "counts" (u64 nl, nh), "heavy" (u32 heavy ids), "light_w", "heavy_w" (f64),
  * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries), "block_totals",

@@ -7,12 +7,13 @@ import os
 import subprocess
 
 from .wrs import (BUCKET_DTYPE, Sampler, Weights, WrsError, default_jobs, last_error, lib,
-                  set_timing, shard_counts, shard_range, shard_seed, status_name)
+                  sample_with_replacement, set_timing, shard_counts, shard_range, shard_seed,
+                  status_name)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 __all__ = ["BUCKET_DTYPE", "Sampler", "Weights", "WrsError", "build", "default_jobs",
-           "last_error", "lib", "set_timing", "shard_counts", "shard_range", "shard_seed",
+           "last_error", "lib", "sample_with_replacement", "set_timing", "shard_counts", "shard_range", "shard_seed",
            "status_name"]
 
 

@@ -214,6 +214,7 @@ struct wrs_sampler {
     std::mutex mu;  // rebuild / stage access
     // draw scratch (region plan), reused across draws; sws_ev orders users
     mutable wrsb::SampleWorkspace sws;
+    mutable wrsb::CountWorkspace cws;  // aggregated draws (guarded by sws_mu)
     mutable std::mutex sws_mu;
     mutable cudaEvent_t sws_ev = nullptr;
     // side stream for the table-independent first stage of a draw (the
@@ -235,6 +236,7 @@ struct wrs_sampler {
             if (e) cudaEventSynchronize(e), cudaEventDestroy(e);
         hi.reset();
         sws.release();
+        cws.release();
         for (cudaEvent_t& e : ev)
             if (e) cudaEventDestroy(e);
     }
@@ -295,6 +297,29 @@ void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, ui
     ck(cudaEventRecord(s.sws_ev, st), "event");
 }
 
+// Aggregated draws on stream st, ordered with the other users of the draw
+// scratch like sample_on (the counting plan has no table-independent prefix
+// worth a side stream: its scatter is a third of the work).
+void count_on(const wrs_sampler& s, uint64_t seed, uint64_t k, uint32_t workers, uint32_t* d_items,
+              uint64_t* d_counts, uint64_t* d_n_unique, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(s.sws_mu);
+    if (!s.sws_ev) {
+        ck(cudaEventCreateWithFlags(&s.sws_ev, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&s.side_ev, cudaEventDisableTiming), "event");
+        s.side = std::make_unique<Stream>(-1);
+    }
+    ck(cudaStreamWaitEvent(st, s.sws_ev, 0), "wait");
+    ck(wrsb::launch_count(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, k, workers, st, &s.sws,
+                          &s.cws, d_items, d_counts,
+                          reinterpret_cast<unsigned long long*>(d_n_unique)),
+       "count launch");
+    ck(cudaEventRecord(s.sws_ev, st), "event");
+}
+
+// Synchronous aggregated draws into host or device buffers of min(k, n).
+void draw_counts(const wrs_sampler& s, uint64_t seed, uint64_t k, unsigned workers,
+                 uint32_t* items, uint64_t* counts, uint64_t* n_unique);
+
 bool is_device_pointer(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -341,6 +366,32 @@ void draw_to_host(const wrs_sampler& s, uint64_t seed, uint64_t count, unsigned 
     }
     ck(cudaStreamSynchronize(copy.s), "draw");
     ck(cudaStreamSynchronize(s.stream->s), "draw");
+}
+
+void draw_counts(const wrs_sampler& s, uint64_t seed, uint64_t k, unsigned workers,
+                 uint32_t* items, uint64_t* counts, uint64_t* n_unique) {
+    const uint64_t cap = std::min(k, s.n);
+    const bool dev = is_device_pointer(items) && is_device_pointer(counts);
+    std::unique_ptr<DevBuf> bi, bc;
+    uint32_t* d_items = items;
+    uint64_t* d_counts = counts;
+    if (!dev) {
+        bi = std::make_unique<DevBuf>(std::max<uint64_t>(cap, 1) * sizeof(uint32_t));
+        bc = std::make_unique<DevBuf>(std::max<uint64_t>(cap, 1) * sizeof(uint64_t));
+        d_items = static_cast<uint32_t*>(bi->p);
+        d_counts = static_cast<uint64_t*>(bc->p);
+    }
+    DevBuf nu(sizeof(uint64_t));
+    count_on(s, seed, k, workers ? workers : 1, d_items, d_counts, static_cast<uint64_t*>(nu.p),
+             s.stream->s);
+    uint64_t m = 0;
+    ck(cudaMemcpyAsync(&m, nu.p, sizeof m, cudaMemcpyDeviceToHost, s.stream->s), "D2H");
+    ck(cudaStreamSynchronize(s.stream->s), "draw counts");
+    if (!dev && m) {
+        ck(cudaMemcpy(items, d_items, m * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(counts, d_counts, m * sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+    }
+    *n_unique = m;
 }
 
 // implied_masses (verify.hpp:43-54): Kahan per item in bucket order, so the
@@ -531,15 +582,23 @@ wrs_status wrs_sampler_draw(const wrs_sampler* s, uint64_t seed, uint64_t count,
 
 void wrs_sampler_free(wrs_sampler* s) { delete s; }
 
+// capi.cpp:222-239 -- bulk with-replacement sample as (item, count) pairs.
+wrs_status wrs_sample_with_replacement(const wrs_weights* w, uint64_t k, uint64_t seed,
+                                       unsigned workers, uint32_t* items, uint64_t* counts,
+                                       uint64_t* n_unique) {
+    if (!w || !items || !counts || !n_unique) return fail(WRS_EINVAL, "null argument");
+    return guarded([&]() -> wrs_status {
+        auto s = build_psa(w->data, wrsb::default_jobs(w->data->n), 0, "psa");
+        draw_counts(*s, seed, k, workers ? workers : 1, items, counts, n_unique);
+        return WRS_OK;
+    });
+}
+
 // ---- outside the hot path --------------------------------------------------------
 static wrs_status not_in_path(const char* what) {
     return fail(WRS_EINVAL, std::string(what) + " is not part of the B200 PSA path");
 }
 
-wrs_status wrs_sample_with_replacement(const wrs_weights*, uint64_t, uint64_t, unsigned,
-                                       uint32_t*, uint64_t*, uint64_t*) {
-    return not_in_path("wrs_sample_with_replacement");
-}
 wrs_status wrs_sample_without_replacement(const wrs_weights*, uint64_t, uint64_t, unsigned,
                                           uint32_t*) {
     return not_in_path("wrs_sample_without_replacement");
@@ -711,6 +770,30 @@ wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t seed, uin
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
         sample_on(*s, seed, 0, count, count, workers ? workers : 1, 0, d_out, st);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_draw_counts(const wrs_sampler* s, uint64_t seed, uint64_t k,
+                                        unsigned workers, uint32_t* items, uint64_t* counts,
+                                        uint64_t* n_unique) {
+    if (!s || !items || !counts || !n_unique) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        draw_counts(*s, seed, k, workers, items, counts, n_unique);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_draw_counts_device(const wrs_sampler* s, uint64_t seed, uint64_t k,
+                                               unsigned workers, uint32_t* d_items,
+                                               uint64_t* d_counts, uint64_t* d_n_unique,
+                                               void* stream) {
+    if (!s || !d_items || !d_counts || !d_n_unique) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        count_on(*s, seed, k, workers ? workers : 1, d_items, d_counts, d_n_unique, st);
         return WRS_OK;
     });
 }

@@ -91,6 +91,24 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
                           cudaEvent_t side_ev = nullptr);
 bool use_region_plan(uint64_t n, uint64_t k);
 
+// Aggregated draws: the (item, count) pairs of sample_many(seed, k, workers)
+// (the same draws as launch_sample), items ascending, into d_items /
+// d_counts (min(k, n) entries) and *d_n_unique (device).  Per-bucket hit
+// counters + fold + compaction; scratch grows on demand.
+struct CountWorkspace {
+    uint32_t* hits = nullptr;             // 2n: own answers per bucket, then alias answers
+    unsigned long long* count = nullptr;  // per item
+    uint32_t* tile_cnt = nullptr;
+    uint64_t* tile_off = nullptr;
+    uint64_t n = 0;
+    cudaError_t reserve(uint64_t n);
+    void release();
+};
+cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
+                         uint64_t stream_id, uint64_t k, uint32_t workers, cudaStream_t st,
+                         SampleWorkspace* ws, CountWorkspace* cw, uint32_t* d_items,
+                         uint64_t* d_counts, unsigned long long* d_n_unique);
+
 // generate_uniform on the device (weight_file.hpp:32-38): counter-based, so
 // every element is independent and bit-exact; items [offset, offset + n) of
 // the global vector (a shard's slice).

@@ -24,6 +24,7 @@
 // No stage needs a host round trip: counts live in DevScalars and every grid
 // is sized from upper bounds.
 #include <atomic>
+#include <type_traits>
 #include <cstdio>
 #include <math_constants.h>
 
@@ -348,7 +349,9 @@ struct K2Lane {
 };
 
 // PASS3 = false: pass 1 (block totals).  PASS3 = true: pass 3 (prefixes).
-template <bool PASS3>
+// CS = CompSumPos when the weights' total is far below DBL_MAX (every chain
+// value is then finite and >= 0), else the guarded CompSum.
+template <bool PASS3, class CS>
 __global__ void __launch_bounds__(K2_WARPS * 32)
 k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
               double* __restrict__ lpre, double* __restrict__ hpre, const DevScalars* sc,
@@ -390,7 +393,7 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
         cp_async_commit();
     };
 
-    CompSum cs{0.0, 0.0};
+    CS cs{0.0, 0.0};
     if (PASS3 && me.len > 0) cs.add(carries[b]);  // run.add(carry[b]), parallel.hpp:124
     load_chunk(0, 0);
     for (int c = 0; c < nchunks; ++c) {
@@ -404,9 +407,29 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
         __syncwarp();
         const int cnt = min(K2_C, me.len - c * K2_C);
         double* row = tile[wq][buf][lane];
-        for (int e = 0; e < cnt; ++e) {
-            cs.add(row[e]);
-            if (PASS3) row[e] = cs.value();  // out[i] = run.value(), :127
+        if (cnt == K2_C) {
+            // full chunk: the running (hi, lo) pairs are kept and the outputs
+            // hi + lo formed after each group of 8 adds, so the output DADDs
+            // do not sit between the adds of the in-order chain
+#pragma unroll
+            for (int e0 = 0; e0 < K2_C; e0 += 8) {
+                double hs[8], ls[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    cs.add(row[e0 + u]);
+                    hs[u] = cs.hi;
+                    ls[u] = cs.lo;
+                }
+                if (PASS3) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) row[e0 + u] = hs[u] + ls[u];  // run.value(), :127
+                }
+            }
+        } else {
+            for (int e = 0; e < cnt; ++e) {
+                cs.add(row[e]);
+                if (PASS3) row[e] = cs.value();  // out[i] = run.value(), :127
+            }
         }
         __syncwarp();
         if (PASS3) {
@@ -429,7 +452,75 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
 //   is unrolled so smem loads and carry stores leave the dependent DADD chain.
 // ===========================================================================
 constexpr int K2B_CHUNK = 1024;
+constexpr int K2B_B = 4;  // adds per software-pipeline stage
 
+// The carry chain for CompSumPos, software-pipelined by hand over blocks of
+// B totals.  Block v goes through three stages in consecutive steps: the hi
+// chain (t = hi + x), the error terms e = (max - t) + min (independent of
+// each other), and the lo chain (lo += e) with the output hi + lo of the
+// state before each add.  Step v runs hi(v), e(v-1), lo(v-2) interleaved add
+// by add, so the in-order warp always has independent FP64 work between the
+// dependent DADDs of each chain.  Exactly the additions of CompSumPos::add, in
+// the same order per chain.  Register sets rotate mod 3 (compile-time via an
+// unroll by 3).  Returns the number of totals consumed; the caller finishes.
+struct ChainRegs {
+    double X[3][K2B_B], H[3][K2B_B], T[3][K2B_B], E[3][K2B_B];
+};
+template <int SH, int SE, int SL, bool DH, bool DE, bool DL>
+__device__ __forceinline__ void chain_step(const double* in, double* out, int v, double& hi,
+                                           double& lo, ChainRegs& R) {
+    constexpr int B = K2B_B;
+    if (DH) {
+#pragma unroll
+        for (int u = 0; u < B; ++u) R.X[SH][u] = in[v * B + u];
+    }
+    double lb[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+        if (DH) {
+            R.H[SH][u] = hi;
+            R.T[SH][u] = hi + R.X[SH][u];
+            hi = R.T[SH][u];
+        }
+        if (DE) {
+            const bool big = R.H[SE][u] >= R.X[SE][u];
+            const double a = big ? R.H[SE][u] : R.X[SE][u], b = big ? R.X[SE][u] : R.H[SE][u];
+            R.E[SE][u] = (a - R.T[SE][u]) + b;
+        }
+        if (DL) {
+            lb[u] = lo;
+            lo = lo + R.E[SL][u];
+        }
+    }
+    if (DL) {
+#pragma unroll
+        for (int u = 0; u < B; ++u) out[(v - 2) * B + u] = R.H[SL][u] + lb[u];  // acc.value()
+    }
+}
+__device__ __forceinline__ int carry_chain_pos(const double* in, double* out, int cnt,
+                                               CompSumPos& acc) {
+    constexpr int B = K2B_B;
+    const int nblk = cnt / B;
+    if (nblk < 5) return 0;
+    double hi = acc.hi, lo = acc.lo;
+    ChainRegs R;
+    chain_step<0, 0, 0, true, false, false>(in, out, 0, hi, lo, R);  // hi(0)
+    chain_step<1, 0, 0, true, true, false>(in, out, 1, hi, lo, R);   // hi(1), e(0)
+    int v = 2;
+    for (; v + 3 <= nblk; v += 3) {
+        chain_step<2, 1, 0, true, true, true>(in, out, v, hi, lo, R);
+        chain_step<0, 2, 1, true, true, true>(in, out, v + 1, hi, lo, R);
+        chain_step<1, 0, 2, true, true, true>(in, out, v + 2, hi, lo, R);
+    }
+    // v = 2 mod 3: block v-2 (set 0) waits for lo, block v-1 (set 1) for e, lo
+    chain_step<0, 1, 0, false, true, true>(in, out, v, hi, lo, R);      // e(v-1), lo(v-2)
+    chain_step<0, 0, 1, false, false, true>(in, out, v + 1, hi, lo, R);  // lo(v-1)
+    acc.hi = hi;
+    acc.lo = lo;
+    return v * B;
+}
+
+template <class CS>
 __global__ void __launch_bounds__(32)
 k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* carries,
              double* lpre, double* hpre) {
@@ -453,7 +544,7 @@ k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* ca
         }
         cp_async_commit();
     };
-    CompSum acc{0.0, 0.0};
+    CS acc{0.0, 0.0};
     load(0, 0);
     for (uint64_t c = 0; c < nchunks; ++c) {
         const int bsel = static_cast<int>(c & 1);
@@ -469,17 +560,23 @@ k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* ca
             double* out = dst + c * K2B_CHUNK;
             const double* in = buf[bsel];
             int i = 0;
+            if constexpr (std::is_same<CS, CompSumPos>::value) {
+                i = carry_chain_pos(in, out, cnt, acc);
+            }
             for (; i + 16 <= cnt; i += 16) {
-                double t[16], v[16];
+                double t[16], hs[16], ls[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) t[u] = in[i + u];
+                // carry[b] = acc.value(), then acc.add(total): keep the (hi, lo)
+                // pairs and form the values after the adds (off the chain)
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    v[u] = acc.value();  // carry[b] = acc.value(), then acc.add(total)
+                    hs[u] = acc.hi;
+                    ls[u] = acc.lo;
                     acc.add(t[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < 16; ++u) out[i + u] = v[u];
+                for (int u = 0; u < 16; ++u) out[i + u] = hs[u] + ls[u];
             }
             for (; i < cnt; ++i) {
                 const double t = in[i];
@@ -912,13 +1009,26 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     k_partition<<<static_cast<unsigned>(ntiles), K1_THREADS, k1_smem, st>>>(
         d_w, n, ntiles, ws.sc, ws.tile_status, ws.lw, ws.hidx, ws.hw);
     REC(1);
-    k_scan_blocks<false><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc,
-                                                            ws.totals, ws.carries);
+    // every prefix-chain value is finite and >= 0 when W is far below DBL_MAX
+    const bool pos = total < 1e300;
+    if (pos)
+        k_scan_blocks<false, CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(
+            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
+    else
+        k_scan_blocks<false, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(
+            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
     REC(2);
-    k_scan_carry<<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
+    if (pos)
+        k_scan_carry<CompSumPos><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
+    else
+        k_scan_carry<CompSum><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     REC(3);
-    k_scan_blocks<true><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc,
-                                                           ws.totals, ws.carries);
+    if (pos)
+        k_scan_blocks<true, CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(
+            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
+    else
+        k_scan_blocks<true, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(
+            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
     REC(4);
     k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
                                      ws.split_s);

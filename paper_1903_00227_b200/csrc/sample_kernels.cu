@@ -295,7 +295,9 @@ __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg) {
     return ((head + 15) & ~size_t(15)) + RS_TILE * sizeof(uint2) + RS_TILE * sizeof(uint16_t);
 }
 
-template <bool W1>
+// ORDER = false (aggregated draws): the answers are only counted, never put
+// back in draw order, so the tile slots and the run table are not written.
+template <bool W1, bool ORDER = true>
 __global__ void __launch_bounds__(RS_THREADS)
 k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restrict__ overflow,
                  uint2* __restrict__ rec, uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
@@ -368,7 +370,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
             const uint32_t slot = loc[reg] + rank[r];
             stage[slot] = make_uint2(t32 + e, bk[r]);
             regmap[slot] = static_cast<uint16_t>(reg);
-            slot_of[tbase + e] = static_cast<uint16_t>(slot);
+            if (ORDER) slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
     }
     // claim slab space for each non-empty run of this tile
@@ -386,7 +388,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
             }
         }
         goff[reg] = g - loc[reg];  // slab position of staged slot i = goff[region] + i
-        runs[tile * rg.nreg + reg] = RunInfo{g, loc[reg]};
+        if (ORDER) runs[tile * rg.nreg + reg] = RunInfo{g, loc[reg]};
     }
     __syncthreads();
     // (no early exit on overflow: an overflowed run is written to the start
@@ -524,6 +526,219 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
     } else {
         for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS)
             out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
+    }
+}
+
+// ===========================================================================
+// aggregated draws: (item, count) pairs of sample_many(seed, k, workers)
+//   The draws are the same as above; only their answers are counted.  Each
+//   bucket b gets two 32-bit counters: draws answered by b itself
+//   (x < share) and draws answered by its alias.  With
+//   the region plan the counters of a region are L2-resident while the
+//   gather sweeps it.  A fold then adds the own count to count[b] and pushes
+//   the alias count to count[alias[b]] (aliases are near b: PSA jobs pair index-
+//   ordered lights and heavies), and a compaction writes the nonzero counts in
+//   item order.  Chunks of <= 2^31 draws keep each counter below 2^32.
+// ===========================================================================
+// hits[0, n): draws answered by bucket b itself; hits[n, 2n): by its alias
+__device__ __forceinline__ void count_hit(uint32_t* hits, uint64_t n, uint32_t b, bool alias) {
+    atomicAdd(hits + (alias ? n + b : b), 1u);
+}
+
+template <bool W1>
+__global__ void __launch_bounds__(256)
+k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
+               const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
+               uint32_t* __restrict__ hits) {
+    if (*overflow) return;  // k_count_direct<.., true> recounts the chunk
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 2048;
+    const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);
+    const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
+    const uint64_t valid_end =
+        slab0 + (slab < rg.nreg ? umin64(cursor[slab], rg.cap) : umin64(cursor[rg.nreg], rg.ov_cap));
+    if (p0 >= valid_end) return;
+    const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+    KeyCache kc;
+    const uint64_t key0 = rng_derive(rg.g.base_key, 0);
+    uint2 r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint64_t p = p0 + u * 256 + threadIdx.x;
+        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
+    }
+    __shared__ uint4 bk_s[8 * 256];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
+                     ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint64_t p = p0 + u * 256 + threadIdx.x;
+        const uint4 bk = bk_s[u * 256 + threadIdx.x];
+        if (p < valid_end) {
+            double x;
+            if (W1) {
+                x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
+            } else {
+                uint32_t w;
+                uint64_t m;
+                locate(rg.g, rg.q0 + r[u].x, w, m);
+                x = draw_coin(rg.g, kc.get(rg.g, w), m);
+            }
+            const double share = __hiloint2double(static_cast<int>(bk.y), static_cast<int>(bk.x));
+            count_hit(hits, rg.g.n, r[u].y, x >= share);  // ia[x >= share]
+        }
+    }
+}
+
+// Direct counting of draws [q_begin, q_end): the whole call when the table
+// is L2-resident, or (IF_OVERFLOW) the region chunk whose slabs overflowed.
+template <bool W1, bool IF_OVERFLOW>
+__global__ void __launch_bounds__(K5_THREADS)
+k_count_direct(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_end,
+               const unsigned* __restrict__ overflow, uint32_t* __restrict__ hits) {
+    if (IF_OVERFLOW && !*overflow) return;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * K5_THREADS;
+    const uint64_t first = q_begin + static_cast<uint64_t>(blockIdx.x) * K5_THREADS + threadIdx.x;
+    DrawCursor<W1> cur;
+    cur.init(g, first < q_end ? first : q_begin);
+    for (uint64_t q = first; q < q_end; q += stride) {
+        const uint64_t c1 = cur.ctr1(g, q);
+        const uint32_t bi = static_cast<uint32_t>(bucket_of_ctr(g, c1));
+        const uint4 bk = ld_bucket(b, bi);
+        const double share = __hiloint2double(static_cast<int>(bk.y), static_cast<int>(bk.x));
+        count_hit(hits, g.n, bi, coin_of_ctr(g, c1) >= share);
+    }
+}
+
+// Fold: count[b] += own[b], count[alias[b]] += alias hits[b], counters reset.
+// Lanes pushing to the same alias (runs of lights share their heavy) combine
+// first, so most alias pushes are one atomic per run.
+__global__ void __launch_bounds__(256)
+k_count_fold(const Bucket* __restrict__ b, uint64_t n, uint32_t* __restrict__ hits,
+             unsigned long long* __restrict__ count) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 256;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * 256; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + threadIdx.x;
+        uint32_t self = 0, al = 0, alias = 0xffffffffu;
+        if (i < n) {
+            self = hits[i];
+            al = hits[n + i];
+            if (self) hits[i] = 0;
+            if (al) {
+                hits[n + i] = 0;
+                alias = b[i].alias;
+            }
+        }
+        if (self) atomicAdd(count + i, static_cast<unsigned long long>(self));
+        const uint32_t key = al ? alias : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const uint32_t sum = __reduce_add_sync(peers, al);
+        if (key != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1)
+            atomicAdd(count + key, static_cast<unsigned long long>(sum));
+    }
+}
+
+// Compaction of the nonzero counts in item order: per-tile counts, one-CTA
+// scan, then each tile writes its (item, count) pairs at its offset.
+constexpr int CC_THREADS = 256;
+constexpr int CC_TILE = CC_THREADS * 16;
+
+__global__ void __launch_bounds__(CC_THREADS)
+k_compact_count(const unsigned long long* __restrict__ count, uint64_t n, uint32_t* __restrict__ tile_cnt) {
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * CC_TILE;
+    uint32_t c = 0;
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+        const uint64_t i = t0 + r * CC_THREADS + threadIdx.x;
+        c += (i < n && count[i] != 0) ? 1u : 0u;
+    }
+    __shared__ uint32_t red[CC_THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < CC_THREADS / 32; ++w) t += red[w];
+        tile_cnt[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+k_compact_scan(const uint32_t* __restrict__ tile_cnt, uint64_t ntiles, uint64_t* __restrict__ tile_off,
+               unsigned long long* __restrict__ n_unique) {
+    __shared__ uint64_t wsum[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t base = 0; base < ntiles; base += 1024) {
+        const uint64_t t = base + threadIdx.x;
+        const uint64_t c = t < ntiles ? tile_cnt[t] : 0;
+        uint64_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint64_t v = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            wsum[lane] = v;
+        }
+        __syncthreads();
+        const uint64_t before = carry + (warp ? wsum[warp - 1] : 0) + x - c;
+        if (t < ntiles) tile_off[t] = before;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = before + c;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_unique = carry;
+}
+
+__global__ void __launch_bounds__(CC_THREADS)
+k_compact_write(const unsigned long long* __restrict__ count, uint64_t n,
+                const uint64_t* __restrict__ tile_off, uint32_t* __restrict__ items,
+                uint64_t* __restrict__ counts) {
+    __shared__ uint32_t wcnt[CC_THREADS / 32];
+    __shared__ uint64_t base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * CC_TILE;
+    if (threadIdx.x == 0) base = tile_off[blockIdx.x];
+    __syncthreads();
+    uint64_t run = base;
+    // rows of CC_THREADS consecutive items, in order
+    for (int r = 0; r < 16; ++r) {
+        const uint64_t i = t0 + r * CC_THREADS + threadIdx.x;
+        const unsigned long long c = i < n ? count[i] : 0ull;
+        const unsigned m = __ballot_sync(0xffffffffu, c != 0);
+        if (lane == 0) wcnt[warp] = __popc(m);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < CC_THREADS / 32; ++w) {
+            const uint32_t v = wcnt[w];
+            before += w < warp ? v : 0;
+            total += v;
+        }
+        if (c) {
+            const uint64_t o = run + before + __popc(m & lanemask_lt());
+            items[o] = static_cast<uint32_t>(i);
+            counts[o] = c;
+        }
+        run += total;
+        __syncthreads();
     }
 }
 
@@ -707,6 +922,114 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+cudaError_t CountWorkspace::reserve(uint64_t need) {
+    if (need <= n && hits) return cudaSuccess;
+    release();
+    const uint64_t nt = (need + CC_TILE - 1) / CC_TILE + 1;
+    cudaError_t e = cudaMalloc(&hits, 2 * need * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&count, need * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&tile_cnt, nt * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&tile_off, nt * sizeof(uint64_t));
+    if (e != cudaSuccess) {
+        release();
+        return e;
+    }
+    n = need;
+    return cudaSuccess;
+}
+
+void CountWorkspace::release() {
+    for (void* p : {static_cast<void*>(hits), static_cast<void*>(count),
+                    static_cast<void*>(tile_cnt), static_cast<void*>(tile_off)})
+        if (p) cudaFree(p);
+    hits = nullptr;
+    count = nullptr;
+    tile_cnt = nullptr;
+    tile_off = nullptr;
+    n = 0;
+}
+
+cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
+                         uint64_t stream_id, uint64_t k, uint32_t workers, cudaStream_t st,
+                         SampleWorkspace* ws, CountWorkspace* cw, uint32_t* d_items,
+                         uint64_t* d_counts, unsigned long long* d_n_unique) {
+    cudaError_t e = cw->reserve(n);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(cw->hits, 0, 2 * n * sizeof(uint32_t), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(cw->count, 0, n * sizeof(unsigned long long), st)) != cudaSuccess) return e;
+    const DrawGeom g = make_geom(n, wn, seed, stream_id, k, workers);
+    const bool w1 = g.W == 1;
+    const bool region = ws && use_region_plan(n, k);
+    constexpr uint64_t kHalf = 1ull << 31;  // per-fold draws: each counter stays < 2^32
+    uint64_t chunk = region ? region_chunk_max() : kHalf;
+    if (chunk > kHalf) chunk = kHalf;
+    if (chunk > k) chunk = k ? k : 1;
+    RegionPlan plan{};
+    RegionBuffers B{};
+    int sm_scatter = 0;
+    if (region) {
+        plan = plan_regions(g, chunk);
+        if ((e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr))) != cudaSuccess) return e;
+        region_bytes(plan, chunk, &B, ws->base);
+        ws->overflow = B.overflow;
+        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg));
+        cudaFuncSetAttribute(k_region_scatter<true, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+        cudaFuncSetAttribute(k_region_scatter<false, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+    }
+    const unsigned fold_blocks = static_cast<unsigned>(
+        umin64((n + 255) / 256, static_cast<uint64_t>(sm_count()) * 8));
+    for (uint64_t c0 = 0; c0 < k; c0 += chunk) {
+        const uint64_t c1 = k - c0 < chunk ? k : c0 + chunk;
+        if (region) {
+            RegionGeom rg = plan.rg;
+            rg.q0 = c0;
+            rg.kc = c1 - c0;
+            rg.ntiles = (rg.kc + RS_TILE - 1) / RS_TILE;
+            if ((e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st)) != cudaSuccess) return e;
+            const unsigned tiles = static_cast<unsigned>(rg.ntiles);
+            const unsigned gblocks = static_cast<unsigned>((plan.rec_slots + 2047) / 2048);
+            const uint64_t span = static_cast<uint64_t>(K5_THREADS);
+            const unsigned dblocks = static_cast<unsigned>(
+                umin64((rg.kc + span - 1) / span, static_cast<uint64_t>(sm_count()) * 8));
+            if (w1) {
+                k_region_scatter<true, false><<<tiles, RS_THREADS, sm_scatter, st>>>(
+                    rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+                k_region_count<true><<<gblocks, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, B.rec,
+                                                              cw->hits);
+                k_count_direct<true, true><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1, B.overflow,
+                                                                           cw->hits);
+            } else {
+                k_region_scatter<false, false><<<tiles, RS_THREADS, sm_scatter, st>>>(
+                    rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+                k_region_count<false><<<gblocks, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, B.rec,
+                                                               cw->hits);
+                k_count_direct<false, true><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1,
+                                                                            B.overflow, cw->hits);
+            }
+        } else {
+            const uint64_t span = static_cast<uint64_t>(K5_THREADS);
+            const unsigned dblocks = static_cast<unsigned>(
+                umin64((c1 - c0 + span - 1) / span, static_cast<uint64_t>(sm_count()) * 8));
+            if (w1)
+                k_count_direct<true, false><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1, nullptr,
+                                                                            cw->hits);
+            else
+                k_count_direct<false, false><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1, nullptr,
+                                                                             cw->hits);
+        }
+        k_count_fold<<<fold_blocks, 256, 0, st>>>(d_b, n, cw->hits, cw->count);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    const uint64_t ntiles = (n + CC_TILE - 1) / CC_TILE;
+    k_compact_count<<<static_cast<unsigned>(ntiles), CC_THREADS, 0, st>>>(cw->count, n, cw->tile_cnt);
+    k_compact_scan<<<1, 1024, 0, st>>>(cw->tile_cnt, ntiles, cw->tile_off, d_n_unique);
+    k_compact_write<<<static_cast<unsigned>(ntiles), CC_THREADS, 0, st>>>(cw->count, n, cw->tile_off,
+                                                                         d_items, d_counts);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_generate_uniform(double* d_w, uint64_t n, uint64_t offset, uint64_t seed,

@@ -40,7 +40,7 @@ SIGNATURES = {
     "wrs_sampler_verify_masses": (C.c_int, [vp, f64]),
     "wrs_sampler_draw": (C.c_int, [vp, u64, u64, C.c_uint, vp]),
     "wrs_sampler_free": (None, [vp]),
-    "wrs_sample_with_replacement": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, vp]),
+    "wrs_sample_with_replacement": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, C.POINTER(u64)]),
     "wrs_sample_without_replacement": (C.c_int, [vp, u64, u64, C.c_uint, vp]),
     "wrs_permutation": (C.c_int, [vp, u64, C.c_uint, vp]),
     "wrs_subset_sample": (C.c_int, [vp, u64, C.c_uint, vp, vp]),
@@ -73,6 +73,8 @@ SIGNATURES = {
     "wrs_b200_shard_counts": (C.c_int, [vp, u64, u64, u64, vp]),
     "wrs_b200_shard_seed": (u64, [u64, u64]),
     "wrs_b200_sampler_draw_shard_device": (C.c_int, [vp, u64, u64, u64, u64, vp, vp]),
+    "wrs_b200_sampler_draw_counts": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, C.POINTER(u64)]),
+    "wrs_b200_sampler_draw_counts_device": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, vp, vp]),
 }
 
 _lib = None
@@ -292,6 +294,23 @@ class Sampler:
         _check(lib().wrs_b200_sampler_draw_shard_device(self.h, seed, shard, count, base,
                                                         _dev_ptr(out), _stream_ptr(stream, out)))
 
+    def draw_counts(self, seed: int, k: int, workers: int = 1) -> tuple[np.ndarray, np.ndarray]:
+        """Distinct items of draw(seed, k, workers) (ascending) and their counts."""
+        cap = max(min(k, self.size), 1)
+        items = np.empty(cap, np.uint32)
+        counts = np.empty(cap, np.uint64)
+        m = u64()
+        _check(lib().wrs_b200_sampler_draw_counts(self.h, seed, k, workers, _ptr(items),
+                                                  _ptr(counts), C.byref(m)))
+        return items[:m.value], counts[:m.value]
+
+    def draw_counts_device(self, seed: int, k: int, workers: int, items, counts, n_unique,
+                           stream=None) -> None:
+        """Device outputs (torch int32 / int64 tensors of min(k, n), n_unique: int64[1])."""
+        _check(lib().wrs_b200_sampler_draw_counts_device(
+            self.h, seed, k, workers, _dev_ptr(items), _dev_ptr(counts), _dev_ptr(n_unique),
+            _stream_ptr(stream, items)))
+
     def stage(self, name: str) -> np.ndarray:
         dtypes = {"counts": np.uint64, "heavy": np.uint32, "light_alias": np.uint32,
                   "heavy_share": np.float64, "heavy_alias": np.uint32,
@@ -339,6 +358,19 @@ def shard_counts(totals, seed: int, k: int) -> np.ndarray:
     out = np.empty(t.size, np.uint64)
     _check(lib().wrs_b200_shard_counts(_ptr(t), t.size, seed, k, _ptr(out)))
     return out
+
+
+def sample_with_replacement(weights: Weights, k: int, seed: int,
+                            workers: int = 1) -> tuple[np.ndarray, np.ndarray]:
+    """wrs_sample_with_replacement: (items, counts) of k draws, items ascending."""
+    n = weights.count()
+    cap = max(min(k, n), 1)
+    items = np.empty(cap, np.uint32)
+    counts = np.empty(cap, np.uint64)
+    m = u64()
+    _check(lib().wrs_sample_with_replacement(weights.h, k, seed, workers, _ptr(items),
+                                             _ptr(counts), C.byref(m)))
+    return items[:m.value], counts[:m.value]
 
 
 def shard_seed(seed: int, shard: int) -> int:

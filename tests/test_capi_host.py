@@ -62,6 +62,10 @@ def test_null_arguments_are_einval():  # capi.cpp:104-105,151-152,208-209
     assert "null" in wrs.last_error()
     assert L.wrs_sampler_build(None, b"psa", 1, 0, C.byref(h)) == WRS_EINVAL
     assert L.wrs_sampler_draw(None, 1, 1, 1, None) == WRS_EINVAL
+    assert L.wrs_sample_with_replacement(None, 1, 1, 1, None, None, None) == WRS_EINVAL
+    assert L.wrs_b200_sampler_draw_counts(None, 1, 1, 1, None, None, None) == WRS_EINVAL
+    assert L.wrs_b200_sampler_draw_counts_device(None, 1, 1, 1, None, None, None,
+                                                 None) == WRS_EINVAL
     assert L.wrs_weights_count(None) == 0
     assert L.wrs_weights_values(None) is None
 
@@ -69,7 +73,6 @@ def test_null_arguments_are_einval():  # capi.cpp:104-105,151-152,208-209
 def test_out_of_path_entry_points_are_stubbed():
     L = lib()
     h = C.c_void_p()
-    assert L.wrs_sample_with_replacement(None, 1, 1, 1, None, None, None) == WRS_EINVAL
     assert L.wrs_permutation(None, 1, 1, None) == WRS_EINVAL
     assert L.wrs_reservoir_create(1, 1, 1, C.byref(h)) == WRS_EINVAL and not h.value
     assert math.isnan(L.wrs_reservoir_threshold(None))
