@@ -122,6 +122,27 @@ WRS_API wrs_status wrs_b200_sampler_draw_shard_device(const wrs_sampler* s, uint
                                                       uint64_t base, uint32_t* d_out,
                                                       void* stream);
 
+/* ------------------------------------------ routed two-level draws (§8f 2)
+ * TwoLevelTable::sample_many(seed, k, workers) (two_level.hpp:66-81),
+ * outputs [q_begin, q_end) into d_out[0 .. q_end - q_begin): per query the
+ * top table (groups buckets, mean top_mean) picks group g, then g's table
+ * (d_tables[g]: sizes[g] buckets of 16 B, mean bucket_means[g]) the local
+ * item; the answer is bases[g] + item.  Tables may be peer-GPU memory (e.g.
+ * opened with wrs_b200_ipc_open): each query then gathers its bucket over
+ * NVLink.  groups <= 256.  Asynchronous on `stream`. */
+WRS_API wrs_status wrs_b200_two_level_draw_device(const void* const* d_tables,
+                                                  const uint64_t* sizes,
+                                                  const double* bucket_means,
+                                                  const uint64_t* bases, uint64_t groups,
+                                                  const void* d_top, double top_mean,
+                                                  uint64_t seed, uint64_t q_begin,
+                                                  uint64_t q_end, uint64_t k, unsigned workers,
+                                                  uint32_t* d_out, void* stream);
+/* CUDA IPC of a sampler's table (handle: 64 bytes), for peer processes. */
+WRS_API wrs_status wrs_b200_sampler_ipc_handle(const wrs_sampler* s, void* handle);
+WRS_API wrs_status wrs_b200_ipc_open(const void* handle, void** d_ptr);
+WRS_API wrs_status wrs_b200_ipc_close(void* d_ptr);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -94,6 +94,8 @@ class Port:
         lib.wo_sample_many.argtypes = [vp, u64, f64, u64, u64, C.c_uint32, vp]
         lib.wo_sample_range.argtypes = [vp, u64, f64, u64, u64, C.c_uint32, u64, u64, vp]
         lib.wo_implied_masses.argtypes = [vp, u64, f64, vp]
+        lib.wo_two_level_sample_range.argtypes = [vp, vp, vp, vp, u64, vp, f64, u64, u64,
+                                                  C.c_uint32, u64, u64, vp]
         lib.wo_max_relative_mass_error.restype = f64
         lib.wo_max_relative_mass_error.argtypes = [vp, vp, u64]
 
@@ -211,6 +213,39 @@ class Port:
         self.lib.wo_implied_masses(_ptr(buckets), buckets.size, wn, _ptr(out))
         return out
 
+    def two_level_build(self, w, groups: int):
+        """TwoLevelTable(wt, psa, 1, groups) (two_level.hpp:30-58) restated:
+        contiguous groups of ceil(n/groups), P=1 psa tables per group and over
+        the group totals.  Returns (tables, means, bases, top, top_mean)."""
+        w = np.ascontiguousarray(w, np.float64)
+        n = w.size
+        groups = min(groups, n)
+        block = -(-n // groups)
+        groups = -(-n // block)
+        bases = [min(n, g * block) for g in range(groups + 1)]
+        tables, means, totals = [], [], []
+        for g in range(groups):
+            wg = w[bases[g]:bases[g + 1]]
+            b, m = self.psa_build(wg, 1)
+            tables.append(b)
+            means.append(m)
+            totals.append(self.pairwise_sum(wg))
+        top, top_mean = self.psa_build(np.array(totals), 1)
+        return tables, np.array(means), np.array(bases[:-1], np.uint64), top, top_mean
+
+    def two_level_sample_range(self, tables, means, bases, top, top_mean, seed, k, workers,
+                               q_lo, q_hi) -> np.ndarray:
+        G = len(tables)
+        ptrs = (C.c_void_p * G)(*[t.ctypes.data for t in tables])
+        sizes = np.array([t.size for t in tables], np.uint64)
+        means = np.ascontiguousarray(means, np.float64)
+        bases = np.ascontiguousarray(bases, np.uint64)
+        out = np.empty(q_hi - q_lo, np.uint32)
+        self.lib.wo_two_level_sample_range(ptrs, _ptr(sizes), _ptr(means), _ptr(bases), G,
+                                           _ptr(top), top_mean, seed, k, workers, q_lo, q_hi,
+                                           _ptr(out))
+        return out
+
     def max_relative_mass_error(self, masses, w) -> float:
         w = np.ascontiguousarray(w, np.float64)
         return self.lib.wo_max_relative_mass_error(_ptr(masses), _ptr(w), w.size)
@@ -257,6 +292,16 @@ class Ref:
         lib.ref_binomial_split.argtypes = [u64, u64, C.c_int64, u64, f64, f64]
         lib.ref_two_level_group_totals.restype = u64
         lib.ref_two_level_group_totals.argtypes = [vp, u64, u64, vp]
+        lib.ref_two_level_new.restype = vp
+        lib.ref_two_level_new.argtypes = [vp, u64, u64]
+        lib.ref_two_level_free.argtypes = [vp]
+        lib.ref_two_level_groups.restype = u64
+        lib.ref_two_level_groups.argtypes = [vp]
+        lib.ref_two_level_group_begin.restype = u64
+        lib.ref_two_level_group_begin.argtypes = [vp, u64]
+        lib.ref_two_level_buckets.restype = u64
+        lib.ref_two_level_buckets.argtypes = [vp, u64, vp, C.POINTER(f64)]
+        lib.ref_two_level_sample_many.argtypes = [vp, u64, u64, C.c_uint, vp]
 
     def generate_uniform(self, n, seed):
         out = np.empty(n, np.float64)
@@ -342,6 +387,42 @@ class Ref:
 
     def binomial_split(self, seed, stream, salt, k, wl, wr):
         return self.lib.ref_binomial_split(seed, stream, salt, k, wl, wr)
+
+    def two_level(self, w, groups):
+        """The reference TwoLevelTable(wt, psa, 1, groups): (tables, means,
+        bases, top, top_mean, draw) with draw(seed, k, workers)."""
+        w = np.ascontiguousarray(w, np.float64)
+        h = self.lib.ref_two_level_new(_ptr(w), w.size, groups)
+        if not h:
+            raise ValueError("reference two-level build failed")
+        try:
+            G = self.lib.ref_two_level_groups(h)
+
+            def buckets(g):
+                m = f64()
+                size = self.lib.ref_two_level_buckets(h, g, None, C.byref(m))
+                b = np.empty(size, BUCKET_DTYPE)
+                self.lib.ref_two_level_buckets(h, g, _ptr(b), C.byref(m))
+                return b, m.value
+            tabs = [buckets(g) for g in range(G)]
+            top, top_mean = buckets(G)
+            bases = np.array([self.lib.ref_two_level_group_begin(h, g) for g in range(G)],
+                             np.uint64)
+        except Exception:
+            self.lib.ref_two_level_free(h)
+            raise
+        lib = self.lib
+
+        class _T:
+            def draw(self_, seed, k, workers):
+                out = np.empty(k, np.uint32)
+                lib.ref_two_level_sample_many(h, seed, k, workers, _ptr(out))
+                return out
+
+            def __del__(self_):
+                lib.ref_two_level_free(h)
+        t = _T()
+        return ([b for b, _ in tabs], np.array([m for _, m in tabs]), bases, top, top_mean, t)
 
     def two_level_group_totals(self, w, groups):
         w = np.ascontiguousarray(w, np.float64)

@@ -252,4 +252,36 @@ uint64_t ref_two_level_group_totals(const double* w, uint64_t n, uint64_t groups
     return t.groups();
 }
 
+/* TwoLevelTable(wt, psa, 1, groups) itself (two_level.hpp:26-58): its local
+ * and top tables and sample_many (:71-81), for the routed-draw pins. */
+void* ref_two_level_new(const double* w, uint64_t n, uint64_t groups) {
+    try {
+        auto wt = table_of(w, n);
+        return new wrs::TwoLevelTable(wt, wrs::AliasTable::Build::psa, 1, groups);
+    } catch (...) {
+        return nullptr;
+    }
+}
+void ref_two_level_free(void* h) { delete static_cast<wrs::TwoLevelTable*>(h); }
+uint64_t ref_two_level_groups(const void* h) {
+    return static_cast<const wrs::TwoLevelTable*>(h)->groups();
+}
+uint64_t ref_two_level_group_begin(const void* h, uint64_t g) {
+    return static_cast<const wrs::TwoLevelTable*>(h)->group_begin(g);
+}
+/* g < groups: local table g; g == groups: the top table.  Returns its size. */
+uint64_t ref_two_level_buckets(const void* h, uint64_t g, void* out, double* mean) {
+    const auto* t = static_cast<const wrs::TwoLevelTable*>(h);
+    const wrs::AliasTable& a = g < t->groups() ? t->local(g) : t->top();
+    if (out) std::memcpy(out, a.buckets().data(), a.size() * sizeof(wrs::alias_bucket));
+    if (mean) *mean = a.bucket_mean();
+    return a.size();
+}
+void ref_two_level_sample_many(const void* h, uint64_t seed, uint64_t k, unsigned workers,
+                               uint32_t* out) {
+    std::vector<uint32_t> v;
+    static_cast<const wrs::TwoLevelTable*>(h)->sample_many(seed, k, workers, v);
+    std::memcpy(out, v.data(), k * sizeof(uint32_t));
+}
+
 } // extern "C"

@@ -460,6 +460,32 @@ void wo_sample_range(const wo_bucket* b, uint64_t n, double wn, uint64_t seed,
     }
 }
 
+/* TwoLevelTable::sample (two_level.hpp:66-69): group by the top table, then
+ * the group's own table; sample_many (:71-81) with RngStream(seed, '2lvl'). */
+void wo_two_level_sample_range(const wo_bucket* const* tables, const uint64_t* sizes,
+                               const double* means, const uint64_t* bases, uint64_t groups,
+                               const wo_bucket* top, double top_mean, uint64_t seed,
+                               uint64_t k, uint32_t workers, uint64_t q_lo, uint64_t q_hi,
+                               uint32_t* out) {
+    if (workers == 0)
+        workers = 1;
+    const wo_rng base = wo_rng_make(seed, 0x326c766cu);
+    for (uint32_t wk = 0; wk < workers; ++wk) {
+        uint64_t lo, hi;
+        worker_slice(k, workers, wk, &lo, &hi);
+        if (hi <= q_lo || lo >= q_hi)
+            continue;
+        wo_rng rng = wo_rng_derive(&base, wk);
+        const uint64_t start = lo > q_lo ? lo : q_lo;
+        const uint64_t end = hi < q_hi ? hi : q_hi;
+        rng.ctr = (start - lo) * 4 * kGolden; /* four outputs per earlier query */
+        for (uint64_t q = start; q < end; ++q) {
+            const uint32_t g = sample_one(top, groups, top_mean, &rng);
+            out[q - q_lo] = (uint32_t)bases[g] + sample_one(tables[g], sizes[g], means[g], &rng);
+        }
+    }
+}
+
 /* -------------------------------------------------------------- verify */
 
 /* kahan_sum: verify.hpp:26-38; implied_masses: verify.hpp:43-54 */

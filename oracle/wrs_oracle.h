@@ -107,6 +107,17 @@ void wo_sample_range(const wo_bucket* b, uint64_t n, double bucket_mean,
                      uint64_t seed, uint64_t k, uint32_t workers, uint64_t q_lo,
                      uint64_t q_hi, uint32_t* out);
 
+/* TwoLevelTable::sample_many (two_level.hpp:66-81), positions [q_lo, q_hi)
+ * of the k outputs: the top table (groups buckets, mean top_mean) picks group
+ * g, table g (sizes[g] buckets, mean means[g]) the local item, output
+ * bases[g] + item; query m of worker w's slice consumes outputs 4m+1..4m+4
+ * of RngStream(seed, 0x326c766c).derive(w). */
+void wo_two_level_sample_range(const wo_bucket* const* tables, const uint64_t* sizes,
+                               const double* means, const uint64_t* bases, uint64_t groups,
+                               const wo_bucket* top, double top_mean, uint64_t seed,
+                               uint64_t k, uint32_t workers, uint64_t q_lo, uint64_t q_hi,
+                               uint32_t* out);
+
 /* implied_masses + max_relative_mass_error (verify.hpp:43-54, 92-98). */
 void wo_implied_masses(const wo_bucket* b, uint64_t n, double bucket_mean, double* m);
 double wo_max_relative_mass_error(const double* m, const double* w, uint64_t n);

@@ -798,6 +798,69 @@ wrs_status wrs_b200_sampler_draw_counts_device(const wrs_sampler* s, uint64_t se
     });
 }
 
+wrs_status wrs_b200_two_level_draw_device(const void* const* d_tables, const uint64_t* sizes,
+                                          const double* bucket_means, const uint64_t* bases,
+                                          uint64_t groups, const void* d_top, double top_mean,
+                                          uint64_t seed, uint64_t q_begin, uint64_t q_end,
+                                          uint64_t k, unsigned workers, uint32_t* d_out,
+                                          void* stream) {
+    if (!d_tables || !sizes || !bucket_means || !bases || !d_top || (!d_out && q_end > q_begin))
+        return fail(WRS_EINVAL, "null argument");
+    if (groups == 0 || groups > static_cast<uint64_t>(wrsb::kTwoLevelMaxGroups))
+        return fail(WRS_EINVAL, "groups must be in [1, 256]");
+    if (q_begin > q_end || q_end > k) return fail(WRS_EINVAL, "bad output range");
+    return guarded([&] {
+        wrsb::TwoLevelDev tl{};
+        for (uint64_t g = 0; g < groups; ++g) {
+            if (!d_tables[g] || sizes[g] == 0 || sizes[g] > 0xffffffffull)
+                throw std::invalid_argument("group tables must be non-empty, < 2^32 buckets");
+            tl.tables[g] = static_cast<const Bucket*>(d_tables[g]);
+            tl.sizes[g] = sizes[g];
+            tl.means[g] = bucket_means[g];
+            tl.bases[g] = bases[g];
+        }
+        tl.top = static_cast<const Bucket*>(d_top);
+        tl.groups = groups;
+        tl.top_mean = top_mean;
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        ck(wrsb::launch_two_level(tl, seed, q_begin, q_end, k, workers ? workers : 1, d_out,
+                                  static_cast<cudaStream_t>(stream)),
+           "two-level launch");
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_ipc_handle(const wrs_sampler* s, void* handle) {
+    if (!s || !handle) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, s->buckets->p), "cudaIpcGetMemHandle");
+        static_assert(sizeof h == 64, "IPC handle is 64 bytes");
+        std::memcpy(handle, &h, sizeof h);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_ipc_open(const void* handle, void** d_ptr) {
+    if (!handle || !d_ptr) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        ck(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_ipc_close(void* d_ptr) {
+    if (!d_ptr) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
+        return WRS_OK;
+    });
+}
+
 // Shard g draws AliasTable(shard_g).sample_many(seed_g, count, 1) with
 // seed_g = RngStream(seed, 'sdrw').derive(g).key, then adds the shard base.
 uint64_t wrs_b200_shard_seed(uint64_t seed, uint64_t shard) {

@@ -109,6 +109,25 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
                          SampleWorkspace* ws, CountWorkspace* cw, uint32_t* d_items,
                          uint64_t* d_counts, unsigned long long* d_n_unique);
 
+// Routed two-level draws (two_level.hpp:66-81): outputs [q_begin, q_end) of
+// TwoLevelTable::sample_many(seed, k, workers) given the group tables (each
+// on this GPU or a peer's, e.g. opened from an IPC handle), their sizes,
+// bucket means and first global ids, and the top table over the group totals.
+constexpr int kTwoLevelMaxGroups = 256;
+struct TwoLevelDev {
+    const Bucket* tables[kTwoLevelMaxGroups];
+    uint64_t sizes[kTwoLevelMaxGroups];
+    double means[kTwoLevelMaxGroups];
+    uint64_t bases[kTwoLevelMaxGroups];
+    const Bucket* top;
+    uint64_t groups;
+    double top_mean;
+};
+constexpr uint64_t kTwoLevelStream = 0x326c766cu;  // "2lvl", two_level.hpp:75
+cudaError_t launch_two_level(const TwoLevelDev& tl, uint64_t seed, uint64_t q_begin,
+                             uint64_t q_end, uint64_t k, uint32_t workers, uint32_t* d_out,
+                             cudaStream_t st);
+
 // generate_uniform on the device (weight_file.hpp:32-38): counter-based, so
 // every element is independent and bit-exact; items [offset, offset + n) of
 // the global vector (a shard's slice).

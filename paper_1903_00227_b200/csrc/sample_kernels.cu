@@ -743,6 +743,50 @@ k_compact_write(const unsigned long long* __restrict__ count, uint64_t n,
 }
 
 // ===========================================================================
+// routed two-level draws (two_level.hpp:66-81)
+//   Query m of worker w's slice consumes outputs 4m+1..4m+4 of
+//   RngStream(seed, '2lvl').derive(w): bucket and coin in the top table pick
+//   group g, bucket and coin in g's table the local item; the answer is
+//   bases[g] + item.  Group tables may live on peer GPUs (NVLink loads).
+// ===========================================================================
+template <bool W1>
+__global__ void __launch_bounds__(256)
+k_two_level_sample(const __grid_constant__ TwoLevelDev tl, DrawGeom g, uint64_t q_begin,
+                   uint64_t q_end, uint32_t* __restrict__ out) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 256;
+    const uint64_t first = q_begin + static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
+    if (first >= q_end) return;
+    uint32_t w;
+    uint64_t m;
+    locate(g, first, w, m);
+    uint64_t lo = first - m;
+    uint64_t hi = W1 ? ~0ull : lo + g.per + (w < g.rem ? 1 : 0);
+    uint64_t key = rng_derive(g.base_key, w);
+    const uint32_t top_n = static_cast<uint32_t>(tl.groups);
+    for (uint64_t q = first; q < q_end; q += stride) {
+        if (!W1) {
+            while (q >= hi) {
+                ++w;
+                lo = hi;
+                hi = lo + g.per + (w < g.rem ? 1 : 0);
+                key = rng_derive(g.base_key, w);
+            }
+        }
+        const uint64_t c = key + (4 * (q - lo) + 1) * kGolden;  // output 4m+1
+        // top table: AliasTable::sample (alias.hpp:265-269)
+        const uint4 tb = ld_bucket(tl.top, mulhi_n32(mix64(c), top_n));
+        const double tx = (static_cast<double>(mix64(c + kGolden) >> 11) * 0x1.0p-53) * tl.top_mean;
+        const uint32_t grp = pick(tb, tx);
+        // the group's own table
+        const uint4 lb = ld_bucket(tl.tables[grp],
+                                   mulhi_n32(mix64(c + 2 * kGolden), static_cast<uint32_t>(tl.sizes[grp])));
+        const double lx =
+            (static_cast<double>(mix64(c + 3 * kGolden) >> 11) * 0x1.0p-53) * tl.means[grp];
+        out[q - q_begin] = static_cast<uint32_t>(tl.bases[grp]) + pick(lb, lx);
+    }
+}
+
+// ===========================================================================
 // host side
 // ===========================================================================
 __global__ void k_generate_uniform(double* __restrict__ w, uint64_t n, uint64_t offset,
@@ -1029,6 +1073,23 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
     k_compact_scan<<<1, 1024, 0, st>>>(cw->tile_cnt, ntiles, cw->tile_off, d_n_unique);
     k_compact_write<<<static_cast<unsigned>(ntiles), CC_THREADS, 0, st>>>(cw->count, n, cw->tile_off,
                                                                          d_items, d_counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_two_level(const TwoLevelDev& tl, uint64_t seed, uint64_t q_begin,
+                             uint64_t q_end, uint64_t k, uint32_t workers, uint32_t* d_out,
+                             cudaStream_t st) {
+    if (q_end <= q_begin) return cudaSuccess;
+    const DrawGeom g = make_geom(tl.groups, tl.top_mean, seed, kTwoLevelStream, k, workers);
+    uint64_t blocks = (q_end - q_begin + 255) / 256;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
+    if (blocks > cap) blocks = cap;
+    if (g.W == 1)
+        k_two_level_sample<true><<<static_cast<unsigned>(blocks), 256, 0, st>>>(tl, g, q_begin,
+                                                                                q_end, d_out);
+    else
+        k_two_level_sample<false><<<static_cast<unsigned>(blocks), 256, 0, st>>>(tl, g, q_begin,
+                                                                                 q_end, d_out);
     return cudaGetLastError();
 }
 

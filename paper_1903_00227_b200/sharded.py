@@ -41,6 +41,21 @@ def default_gather(local_total: float) -> np.ndarray:
     return out.cpu().numpy()
 
 
+def default_gather_obj(obj) -> list:
+    """All-gather one picklable object per rank with torch.distributed."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def worker_slice(k: int, workers: int, w: int) -> tuple[int, int]:
+    """parallel.hpp:37-43."""
+    per, rem = divmod(k, workers)
+    lo = per * w + min(w, rem)
+    return lo, lo + per + (1 if w < rem else 0)
+
+
 class ShardedSampler:
     """One rank's part of a sharded PSA sampler.
 
@@ -76,3 +91,43 @@ class ShardedSampler:
         table over the gathered shard totals, built identically on every rank."""
         self._top_w = _w.Weights.from_array(self.totals)
         return _w.Sampler.build(self._top_w, "psa", 1)
+
+    # ---- routed two-level draws (SURVEY §8f row 2) ---------------------------
+    def open_peers(self, gather_obj: Callable[[object], list] = default_gather_obj) -> None:
+        """Exchange every shard table's CUDA IPC handle, size and bucket mean
+        and open the peers' tables in this process (their buckets are then
+        read over NVLink by the routed draw)."""
+        meta = (_w.ipc_handle(self.sampler), self.sampler.size, self.sampler.bucket_mean)
+        metas = gather_obj(meta)
+        self._peer_ptrs = []
+        self._opened = []
+        for r, (h, _, _) in enumerate(metas):
+            if r == self.rank:
+                self._peer_ptrs.append(self.sampler.device_buckets())
+            else:
+                p = _w.ipc_open(h)
+                self._opened.append(p)
+                self._peer_ptrs.append(p)
+        self._sizes = np.array([m[1] for m in metas], np.uint64)
+        self._means = np.array([m[2] for m in metas], np.float64)
+        self._bases = np.array([shard_of(self.n_total, self.world, r)[0]
+                                for r in range(self.world)], np.uint64)
+        self._top = self.top_table()
+
+    def routed_draw_device(self, seed: int, k: int, out, stream=None) -> tuple[int, int]:
+        """Worker `rank` of `world` of TwoLevelTable::sample_many(seed, k, world)
+        (two_level.hpp:71-81) over the shard tables: rows [q0, q1) of the global
+        output into out[0 .. q1 - q0).  Every query picks its shard with the top
+        table and gathers from that shard's table, wherever it lives."""
+        if not hasattr(self, "_peer_ptrs"):
+            raise RuntimeError("open_peers() first")
+        q0, q1 = worker_slice(k, self.world, self.rank)
+        _w.two_level_draw_device(self._peer_ptrs, self._sizes, self._means, self._bases,
+                                 self._top.device_buckets(), self._top.bucket_mean, seed, q0, q1,
+                                 k, self.world, out, stream)
+        return q0, q1
+
+    def close_peers(self) -> None:
+        for p in getattr(self, "_opened", []):
+            _w.ipc_close(p)
+        self._opened = []

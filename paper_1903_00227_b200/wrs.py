@@ -74,6 +74,11 @@ SIGNATURES = {
     "wrs_b200_shard_seed": (u64, [u64, u64]),
     "wrs_b200_sampler_draw_shard_device": (C.c_int, [vp, u64, u64, u64, u64, vp, vp]),
     "wrs_b200_sampler_draw_counts": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, C.POINTER(u64)]),
+    "wrs_b200_two_level_draw_device": (C.c_int, [vp, vp, vp, vp, u64, vp, f64, u64, u64, u64,
+                                                 u64, C.c_uint, vp, vp]),
+    "wrs_b200_sampler_ipc_handle": (C.c_int, [vp, vp]),
+    "wrs_b200_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
+    "wrs_b200_ipc_close": (C.c_int, [vp]),
     "wrs_b200_sampler_draw_counts_device": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, vp, vp]),
 }
 
@@ -371,6 +376,39 @@ def sample_with_replacement(weights: Weights, k: int, seed: int,
     _check(lib().wrs_sample_with_replacement(weights.h, k, seed, workers, _ptr(items),
                                              _ptr(counts), C.byref(m)))
     return items[:m.value], counts[:m.value]
+
+
+def two_level_draw_device(tables, sizes, means, bases, top, top_mean: float, seed: int,
+                          q_begin: int, q_end: int, k: int, workers: int, out,
+                          stream=None) -> None:
+    """wrs_b200_two_level_draw_device: outputs [q_begin, q_end) of
+    TwoLevelTable::sample_many(seed, k, workers) into `out` (device).
+    `tables` / `top`: device pointers (ints) or CUDA tensors."""
+    G = len(tables)
+    ptrs = (vp * G)(*[t if isinstance(t, int) else _dev_ptr(t) for t in tables])
+    sz = np.ascontiguousarray(sizes, np.uint64)
+    mn = np.ascontiguousarray(means, np.float64)
+    bs = np.ascontiguousarray(bases, np.uint64)
+    tp = top if isinstance(top, int) else _dev_ptr(top)
+    _check(lib().wrs_b200_two_level_draw_device(ptrs, _ptr(sz), _ptr(mn), _ptr(bs), G, tp,
+                                                top_mean, seed, q_begin, q_end, k, workers,
+                                                _dev_ptr(out), _stream_ptr(stream, out)))
+
+
+def ipc_handle(sampler: "Sampler") -> bytes:
+    buf = (C.c_char * 64)()
+    _check(lib().wrs_b200_sampler_ipc_handle(sampler.h, buf))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    p = vp()
+    _check(lib().wrs_b200_ipc_open(C.c_char_p(handle), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().wrs_b200_ipc_close(vp(ptr)))
 
 
 def shard_seed(seed: int, shard: int) -> int:

@@ -139,8 +139,30 @@ def main():
     r["alia_s99_d0"] = R.rng_outputs(99, 0x616C6961, 0, 64)
     r["alia_s99_d3"] = R.rng_outputs(99, 0x616C6961, 3, 64)
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **r)
+    two_level(R)
     print("golden fixtures written to", HERE)
 
 
+def two_level(R):
+    """TwoLevelTable(wt, psa, 1, G).sample_many (two_level.hpp:26-81) over
+    generate_powerlaw(3001, 1.0, 5): the routed-draw pins."""
+    t = {}
+    w = R.generate_powerlaw(3001, 1.0, 5)
+    t["w_sha"] = sha(w)
+    for G in (4, 7):
+        tabs, means, bases, top, top_mean, T = R.two_level(w, G)
+        t[f"G{G}/bases"] = bases
+        t[f"G{G}/means"] = means
+        t[f"G{G}/top"] = top
+        t[f"G{G}/top_mean"] = np.float64(top_mean)
+        t[f"G{G}/tables_sha"] = sha(np.concatenate(tabs))
+        for W in (1, 3):
+            t[f"G{G}/draws_s7_k5001_W{W}"] = T.draw(7, 5001, W)
+    np.savez_compressed(os.path.join(HERE, "two_level.npz"), **t)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["two_level"]:
+        two_level(oracle.ref())
+    else:
+        main()

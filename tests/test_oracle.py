@@ -187,3 +187,18 @@ def test_oracle_draws_follow_weights(P):  # test_alias.cpp:269-284
     s = P.sample_many(b, wn, 99, 100001, 4)
     counts = np.bincount(s, minlength=50)
     assert chi_square(counts, w / w.sum())[3]
+
+
+def test_golden_two_level(P):  # TwoLevelTable (two_level.hpp:26-81), reference-generated
+    t = np.load(os.path.join(GOLD, "two_level.npz"))
+    w = P.generate_powerlaw(3001, 1.0, 5)
+    assert hashlib.sha256(w.tobytes()).hexdigest() == str(t["w_sha"])
+    for G in (4, 7):
+        tabs, means, bases, top, tm = P.two_level_build(w, G)
+        assert np.array_equal(bases, t[f"G{G}/bases"])
+        assert np.array_equal(means, t[f"G{G}/means"])
+        assert top.tobytes() == t[f"G{G}/top"].tobytes() and tm == float(t[f"G{G}/top_mean"])
+        assert hashlib.sha256(np.concatenate(tabs).tobytes()).hexdigest() == str(t[f"G{G}/tables_sha"])
+        for W in (1, 3):
+            got = P.two_level_sample_range(tabs, means, bases, top, tm, 7, 5001, W, 0, 5001)
+            assert np.array_equal(got, t[f"G{G}/draws_s7_k5001_W{W}"])

@@ -76,3 +76,20 @@ def test_port_equals_reference_generators_and_masses():
     assert P.implied_masses(b, wn).tobytes() == R.implied_masses(b, wn).tobytes()
     x = np.random.default_rng(3).random(9000)
     assert np.array_equal(P.prefix_sums(x), R.prefix_sums(x, 7))
+
+
+def test_port_equals_reference_two_level():  # two_level.hpp:26-81
+    P = oracle.port()
+    for w in (P.generate_powerlaw(3001, 1.0, 5), P.generate_uniform(1000, 3), np.array([2.0, 1.0])):
+        for G in (1, 2, 3, 7, 64):
+            tabs, means, bases, top, tm = P.two_level_build(w, G)
+            rt, rm, rb, rtop, rtm, T = R.two_level(w, G)
+            assert [t.tobytes() for t in tabs] == [t.tobytes() for t in rt]
+            assert np.array_equal(means, rm) and np.array_equal(bases, rb)
+            assert top.tobytes() == rtop.tobytes() and tm == rtm
+            for W in (1, 3, 8):
+                ref = T.draw(11, 9001, W)
+                assert np.array_equal(P.two_level_sample_range(tabs, means, bases, top, tm, 11,
+                                                               9001, W, 0, 9001), ref)
+                assert np.array_equal(P.two_level_sample_range(tabs, means, bases, top, tm, 11,
+                                                               9001, W, 777, 5000), ref[777:5000])
