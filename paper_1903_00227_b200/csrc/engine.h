@@ -11,11 +11,21 @@
 namespace wrsb {
 
 // PSA job count used by algo "psa": one job = one thread's sequential pack
-// chain, so P sets the build's parallelism.  Fixed per n (DESIGN.md "Job
-// count") so tables are reproducible on any GPU and launch shape.
-constexpr uint64_t kJobBuckets = 1024;
+// chain, so P sets the build's parallelism and the job length its latency.
+// Jobs of J = n / 49152 items rounded down to a power of two, clamped to
+// [32, 1024]: large tables (n >= ~5e7) get 1024-item jobs (~1e5 chains for
+// 148 SMs), smaller ones shorter chains so there are still ~5e4 of them.  A
+// function of n only, so tables are reproducible on
+// any GPU and launch shape.
+constexpr uint64_t kJobBucketsMax = 1024, kJobBucketsMin = 32, kJobTarget = 49152;
+inline uint64_t default_job_items(uint64_t n) {
+    uint64_t j = kJobBucketsMin;
+    while (j < kJobBucketsMax && 2 * j <= n / kJobTarget) j *= 2;
+    return j;
+}
 inline uint64_t default_jobs(uint64_t n) {
-    const uint64_t p = (n + kJobBuckets - 1) / kJobBuckets;
+    const uint64_t j = default_job_items(n);
+    const uint64_t p = (n + j - 1) / j;
     return p ? p : 1;
 }
 

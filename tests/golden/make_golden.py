@@ -98,7 +98,16 @@ def main():
     d["seed100_W4"] = t.sample_many(100, 100001, 4)
     np.savez_compressed(os.path.join(HERE, "draws_small.npz"), **d)
 
-    # --- medium tables at GPU-sized job counts: digests only ---------------
+    medium(R)
+
+    # --- rng known answers (rng.hpp) ----------------------------------------
+    rng_and_two_level(R)
+    print("golden fixtures written to", HERE)
+
+
+def medium(R):
+    """Medium tables at GPU-sized job counts (incl. wrs_b200_default_jobs(n):
+    jobs of 32 items at these n): digests only."""
     m = {}
     for tag, w in (("uniform_1e6_s42", R.generate_uniform(10**6, 42)),
                    ("powerlaw1_1e6_s42", R.generate_powerlaw(10**6, 1.0, 42)),
@@ -114,7 +123,8 @@ def main():
         m[f"{tag}/light_prefix_sha"] = sha(part["light_prefix"])
         m[f"{tag}/heavy_prefix_sha"] = sha(part["heavy_prefix"])
         n = w.size
-        for P in sorted({8, -(-n // 1024), -(-n // 512), -(-n // 256), -(-n // 128)}):
+        for P in sorted({8, -(-n // 1024), -(-n // 512), -(-n // 256), -(-n // 128),
+                         -(-n // 32)}):
             b, wn = R.psa_build_jobs(w, P, 8)
             m[f"{tag}/P{P}/buckets_sha"] = sha(b)
             m[f"{tag}/P{P}/bucket_mean"] = np.float64(wn)
@@ -132,7 +142,8 @@ def main():
     m["uniform_1e8_s42/w_sha"] = sha(R.generate_uniform(10**8, 42))
     np.savez_compressed(os.path.join(HERE, "psa_medium.npz"), **m)
 
-    # --- rng known answers (rng.hpp) ----------------------------------------
+
+def rng_and_two_level(R):
     r = {}
     r["s42_st7"] = R.rng_outputs(42, 7, -1, 64)
     r["s9_st3_d123"] = R.rng_outputs(9, 3, 123, 64)
@@ -140,7 +151,6 @@ def main():
     r["alia_s99_d3"] = R.rng_outputs(99, 0x616C6961, 3, 64)
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **r)
     two_level(R)
-    print("golden fixtures written to", HERE)
 
 
 def two_level(R):
@@ -164,5 +174,7 @@ def two_level(R):
 if __name__ == "__main__":
     if sys.argv[1:] == ["two_level"]:
         two_level(oracle.ref())
+    elif sys.argv[1:] == ["medium"]:
+        medium(oracle.ref())
     else:
         main()

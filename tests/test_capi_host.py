@@ -81,10 +81,15 @@ def test_out_of_path_entry_points_are_stubbed():
 
 
 def test_default_job_count():
+    # jobs of J = pow2_floor(n / 49152) items clamped to [32, 1024]
     assert wrs.default_jobs(1) == 1
-    assert wrs.default_jobs(1024) == 1
-    assert wrs.default_jobs(1025) == 2
+    assert wrs.default_jobs(32) == 1
+    assert wrs.default_jobs(33) == 2
+    assert wrs.default_jobs(10**6) == -(-10**6 // 32)
+    assert wrs.default_jobs(1 << 22) == (1 << 22) // 64
+    assert wrs.default_jobs(1 << 24) == (1 << 24) // 256
     assert wrs.default_jobs(10**8) == -(-10**8 // 1024)
+    assert wrs.default_jobs(1 << 30) == (1 << 30) // 1024
 
 
 def test_shard_ranges_match_two_level_blocks():  # two_level.hpp:33-41
