@@ -58,6 +58,13 @@ WRS_API wrs_status wrs_b200_sampler_copy_buckets(const wrs_sampler* s, void* hos
  * asynchronously on `stream`; no host synchronisation.  Plan errors are
  * latched on the device and reported by wrs_b200_sampler_check. */
 WRS_API wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream);
+/* Give the sampler a second table: from then on a rebuild writes the table
+ * the draws are not reading (after the draws that last read it finish) and
+ * does not hold up `stream`; draws issued after it read the new table (they
+ * wait for it on their own stream).  Lets a rebuild on one stream overlap the
+ * draws of the previous table on another.  Table pointers / IPC handles then
+ * refer to the table current at the time of the call. */
+WRS_API wrs_status wrs_b200_sampler_double_buffer(wrs_sampler* s);
 WRS_API wrs_status wrs_b200_sampler_check(const wrs_sampler* s);
 
 /* Draw into device memory, asynchronously on `stream`.  Same values as

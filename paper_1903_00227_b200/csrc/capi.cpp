@@ -239,8 +239,26 @@ struct wrs_sampler {
         cws.release();
         for (cudaEvent_t& e : ev)
             if (e) cudaEventDestroy(e);
+        for (int b = 0; b < 2; ++b) {
+            if (built_ev[b]) cudaEventSynchronize(built_ev[b]), cudaEventDestroy(built_ev[b]);
+            if (read_ev[b]) cudaEventSynchronize(read_ev[b]), cudaEventDestroy(read_ev[b]);
+        }
     }
-    Bucket* d_b() const { return static_cast<Bucket*>(buckets->p); }
+    // Double-buffered tables (wrs_b200_sampler_double_buffer): rebuilds write
+    // the back table while draws already issued still read the front one;
+    // built_ev[b] marks table b written, read_ev[b] the end of the last draw
+    // that read it.  `front` flips when a rebuild is issued.
+    std::unique_ptr<DevBuf> buckets2;
+    std::atomic<int> front{0};
+    bool dbuf = false;
+    mutable cudaEvent_t built_ev[2] = {};
+    mutable cudaEvent_t read_ev[2] = {};
+    Bucket* table(int b) const { return static_cast<Bucket*>((b ? buckets2 : buckets)->p); }
+    Bucket* d_b() const { return table(front.load()); }
+    // host-side accesses of the front table wait for the rebuild that wrote it
+    void sync_table() const {
+        if (dbuf) ck(cudaEventSynchronize(built_ev[front.load()]), "table ready");
+    }
 };
 
 namespace {
@@ -291,10 +309,13 @@ void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, ui
     }
     ck(cudaStreamWaitEvent(st, s.sws_ev, 0), "wait");
     ck(cudaStreamWaitEvent(s.side->s, s.sws_ev, 0), "wait");
-    ck(wrsb::launch_sample(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, q0, q1, k, workers, base,
-                           out, st, &s.sws, s.side->s, s.side_ev),
+    const int tb = s.front.load();
+    if (s.dbuf) ck(cudaStreamWaitEvent(st, s.built_ev[tb], 0), "wait");
+    ck(wrsb::launch_sample(s.table(tb), s.n, s.wn, seed, wrsb::kSampleStream, q0, q1, k, workers,
+                           base, out, st, &s.sws, s.side->s, s.side_ev),
        "K5 launch");
     ck(cudaEventRecord(s.sws_ev, st), "event");
+    if (s.dbuf) ck(cudaEventRecord(s.read_ev[tb], st), "event");
 }
 
 // Aggregated draws on stream st, ordered with the other users of the draw
@@ -309,11 +330,14 @@ void count_on(const wrs_sampler& s, uint64_t seed, uint64_t k, uint32_t workers,
         s.side = std::make_unique<Stream>(-1);
     }
     ck(cudaStreamWaitEvent(st, s.sws_ev, 0), "wait");
-    ck(wrsb::launch_count(s.d_b(), s.n, s.wn, seed, wrsb::kSampleStream, k, workers, st, &s.sws,
-                          &s.cws, d_items, d_counts,
+    const int tb = s.front.load();
+    if (s.dbuf) ck(cudaStreamWaitEvent(st, s.built_ev[tb], 0), "wait");
+    ck(wrsb::launch_count(s.table(tb), s.n, s.wn, seed, wrsb::kSampleStream, k, workers, st,
+                          &s.sws, &s.cws, d_items, d_counts,
                           reinterpret_cast<unsigned long long*>(d_n_unique)),
        "count launch");
     ck(cudaEventRecord(s.sws_ev, st), "event");
+    if (s.dbuf) ck(cudaEventRecord(s.read_ev[tb], st), "event");
 }
 
 // Synchronous aggregated draws into host or device buffers of min(k, n).
@@ -399,6 +423,7 @@ void draw_counts(const wrs_sampler& s, uint64_t seed, uint64_t k, unsigned worke
 // path; runs over a D2H copy of the table.
 double max_rel_mass_error(const wrs_sampler& s) {
     std::vector<Bucket> b(s.n);
+    s.sync_table();
     ck(cudaMemcpy(b.data(), s.d_b(), s.n * sizeof(Bucket), cudaMemcpyDeviceToHost), "table D2H");
     std::vector<double> sum(s.n, 0.0), comp(s.n, 0.0);
     auto kadd = [&](uint32_t i, double x) {
@@ -707,6 +732,7 @@ wrs_status wrs_b200_sampler_copy_buckets(const wrs_sampler* s, void* host_out) {
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         ck(cudaStreamSynchronize(s->stream->s), "sync");
+        s->sync_table();
         ck(cudaMemcpy(host_out, s->d_b(), s->n * sizeof(Bucket), cudaMemcpyDeviceToHost), "D2H");
         return WRS_OK;
     });
@@ -731,11 +757,44 @@ wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream) {
         }
         ck(cudaEventRecord(s->hi_ev[0], st), "event");
         ck(cudaStreamWaitEvent(s->hi->s, s->hi_ev[0], 0), "wait");
+        if (s->dbuf) {
+            // into the back table, once the draws reading it are done; draws
+            // issued from now on read it (they wait for built_ev themselves)
+            std::lock_guard<std::mutex> g2(s->sws_mu);
+            const int X = 1 - s->front.load();
+            ck(cudaStreamWaitEvent(s->hi->s, s->read_ev[X], 0), "wait");
+            ck(wrsb::launch_psa_build(s->weights->d_w, s->n, s->weights->total, s->P,
+                                      s->table(X), s->ws, s->hi->s, s->timed ? s->ev : nullptr),
+               "PSA launch");
+            ck(cudaEventRecord(s->built_ev[X], s->hi->s), "event");
+            s->front.store(X);
+            return WRS_OK;
+        }
         ck(wrsb::launch_psa_build(s->weights->d_w, s->n, s->weights->total, s->P, s->d_b(),
                                   s->ws, s->hi->s, s->timed ? s->ev : nullptr),
            "PSA launch");
         ck(cudaEventRecord(s->hi_ev[1], s->hi->s), "event");
         ck(cudaStreamWaitEvent(st, s->hi_ev[1], 0), "wait");
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_double_buffer(wrs_sampler* s) {
+    if (!s) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(s->mu);
+        std::lock_guard<std::mutex> g2(s->sws_mu);
+        if (s->dbuf) return WRS_OK;
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        s->buckets2 = std::make_unique<DevBuf>(s->n * sizeof(Bucket));
+        for (int b = 0; b < 2; ++b) {
+            ck(cudaEventCreateWithFlags(&s->built_ev[b], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&s->read_ev[b], cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(s->built_ev[b], s->stream->s), "event");
+            ck(cudaEventRecord(s->read_ev[b], s->stream->s), "event");
+        }
+        s->dbuf = true;
         return WRS_OK;
     });
 }
@@ -836,7 +895,7 @@ wrs_status wrs_b200_sampler_ipc_handle(const wrs_sampler* s, void* handle) {
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         cudaIpcMemHandle_t h;
-        ck(cudaIpcGetMemHandle(&h, s->buckets->p), "cudaIpcGetMemHandle");
+        ck(cudaIpcGetMemHandle(&h, s->d_b()), "cudaIpcGetMemHandle");
         static_assert(sizeof h == 64, "IPC handle is 64 bytes");
         std::memcpy(handle, &h, sizeof h);
         return WRS_OK;

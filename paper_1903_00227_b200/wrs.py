@@ -65,6 +65,7 @@ SIGNATURES = {
     "wrs_b200_sampler_copy_buckets": (C.c_int, [vp, vp]),
     "wrs_b200_sampler_rebuild_async": (C.c_int, [vp, vp]),
     "wrs_b200_sampler_check": (C.c_int, [vp]),
+    "wrs_b200_sampler_double_buffer": (C.c_int, [vp]),
     "wrs_b200_sampler_draw_device": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp]),
     "wrs_b200_sampler_stage": (C.c_int, [vp, C.c_char_p, vp, u64, C.POINTER(u64)]),
     "wrs_b200_set_timing": (C.c_int, [C.c_int]),
@@ -289,6 +290,10 @@ class Sampler:
 
     def check(self) -> None:
         _check(lib().wrs_b200_sampler_check(self.h))
+
+    def double_buffer(self) -> None:
+        """wrs_b200_sampler_double_buffer: rebuilds write a second table."""
+        _check(lib().wrs_b200_sampler_double_buffer(self.h))
 
     def draw_device(self, seed: int, count: int, workers: int, out, stream=None) -> None:
         _check(lib().wrs_b200_sampler_draw_device(self.h, seed, count, workers,

@@ -305,3 +305,24 @@ def test_region_plan_draws_bit_exact(P, chunk, monkeypatch):
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref), (k, Wk)
     # host output path (chunked D2H) through the reference ABI call
     assert np.array_equal(S.draw(5, 6_000_011, 2), P.sample_many(b, S.bucket_mean, 5, 6_000_011, 2))
+
+
+def test_double_buffered_rebuild_then_draw_on_other_stream(P):
+    """wrs_b200_sampler_double_buffer: the first rebuild writes the second
+    (uninitialised) table on its own stream while a draw issued right after it
+    on another stream must wait for it; then pipelined rebuild/draw rounds."""
+    import torch
+    n, k = 3_000_017, 4_000_003
+    w = P.generate_uniform(n, 17)
+    W, S = build(w)
+    ref = P.sample_many(S.buckets(), S.bucket_mean, 5, k, 1)
+    S.double_buffer()
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    out = torch.empty(k, dtype=torch.int32, device="cuda")
+    for i in range(3):
+        S.rebuild_async(a)
+        S.draw_device(5, k, 1, out, b)
+        b.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref), i
+    S.check()
+    assert_same_table(S, w, S.jobs, P)
