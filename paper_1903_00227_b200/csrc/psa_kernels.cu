@@ -311,7 +311,8 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
             }
         }
     }
-    __syncthreads();
+    // the tile-local compaction does not need the look-back's result: the
+    // other warps do it while warp 0 waits on its predecessors
     const uint32_t totL = C.totL, totH = C.totH;
     const unsigned lt = lanemask_lt();
 #pragma unroll

@@ -71,6 +71,49 @@ __global__ void k_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint
     }
 }
 
+// Mixed: warp 0 gathers the first TMA_ROWS of each batch with TMA gather4
+// (lane 0 issues), the other warps gather the rest with LDGSTS -- do the two
+// paths add up?
+template <int TMA_ROWS>
+__global__ void k_mixed(const __grid_constant__ CUtensorMap tmap, const uint4* __restrict__ t, uint32_t n,
+                        uint64_t k, uint32_t* out) {
+    __shared__ __align__(128) uint4 buf[BATCH * 2];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    unsigned phase = 0;
+    for (uint64_t b0 = blockIdx.x * (uint64_t)BATCH; b0 < k; b0 += gridDim.x * (uint64_t)BATCH) {
+        if (threadIdx.x == 0) mbar_expect(&bar, TMA_ROWS * 16);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            for (int g = threadIdx.x; g < TMA_ROWS / 4; g += 32) {
+                int r[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) r[u] = (int)__umulhi(hash32(b0 + g * 4 + u), n);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+                    "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                    ::"r"((unsigned)__cvta_generic_to_shared(&buf[g * 8])), "l"(&tmap), "r"(0), "r"(r[0]),
+                      "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"((unsigned)__cvta_generic_to_shared(&bar))
+                    : "memory");
+            }
+        } else {
+            for (int i = TMA_ROWS + threadIdx.x - 32; i < BATCH; i += blockDim.x - 32) {
+                const uint32_t r = __umulhi(hash32(b0 + i), n);
+                const unsigned s = (unsigned)__cvta_generic_to_shared(&buf[(i / 4) * 8 + (i % 4)]);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(t + r));
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        __syncthreads();
+        for (int i = threadIdx.x; i < BATCH; i += blockDim.x) out[b0 + i] = buf[(i / 4) * 8 + (i % 4)].x ^ buf[(i / 4) * 8 + (i % 4)].w;
+        __syncthreads();
+    }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -120,6 +163,10 @@ int main() {
     time("tma gather4 x1 issuer", [&] { k_tma<1><<<sms * 6, 128>>>(tm, n, k, out); });
     time("tma gather4 x32 issuers", [&] { k_tma<32><<<sms * 6, 128>>>(tm, n, k, out); });
     time("tma gather4 x128 issuers", [&] { k_tma<128><<<sms * 6, 128>>>(tm, n, k, out); });
+    time("ldgsts only (mixed<0>)", [&] { k_mixed<0><<<sms * 6, 256>>>(tm, t, n, k, out); });
+    time("mixed 256 tma / 768 ldgsts", [&] { k_mixed<256><<<sms * 6, 256>>>(tm, t, n, k, out); });
+    time("mixed 384 tma / 640 ldgsts", [&] { k_mixed<384><<<sms * 6, 256>>>(tm, t, n, k, out); });
+    time("mixed 512 tma / 512 ldgsts", [&] { k_mixed<512><<<sms * 6, 256>>>(tm, t, n, k, out); });
     uint32_t v0;
     cudaMemcpy(&v0, out + 12345, 4, cudaMemcpyDeviceToHost);
     printf("check %u %u\n", ref0, v0);
