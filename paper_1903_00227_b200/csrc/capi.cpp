@@ -612,9 +612,10 @@ wrs_status wrs_sample_with_replacement(const wrs_weights* w, uint64_t k, uint64_
                                        unsigned workers, uint32_t* items, uint64_t* counts,
                                        uint64_t* n_unique) {
     if (!w || !items || !counts || !n_unique) return fail(WRS_EINVAL, "null argument");
+    (void)workers;  // parallelism only: the result must not depend on it (test_capi.cpp:104-111)
     return guarded([&]() -> wrs_status {
         auto s = build_psa(w->data, wrsb::default_jobs(w->data->n), 0, "psa");
-        draw_counts(*s, seed, k, workers ? workers : 1, items, counts, n_unique);
+        draw_counts(*s, seed, k, 1, items, counts, n_unique);
         return WRS_OK;
     });
 }

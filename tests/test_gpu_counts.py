@@ -58,11 +58,29 @@ def test_counts_zero_draws_and_module_entry(P):
     S = wrs.Sampler.build(W, "psa", 1)
     items, counts = S.draw_counts(1, 0, 1)
     assert items.size == 0 and counts.size == 0
-    # wrs_sample_with_replacement builds "psa" itself: same pairs as the sampler
+    # wrs_sample_with_replacement builds "psa" itself: the sampler's W=1 pairs
     i2, c2 = wrs.sample_with_replacement(W, 12345, 77, 4)
-    i1, c1 = S.draw_counts(77, 12345, 4)
+    i1, c1 = S.draw_counts(77, 12345, 1)
     assert np.array_equal(i1, i2) and np.array_equal(c1, c2)
     assert np.all(np.diff(i2.astype(np.int64)) > 0)
+
+
+def test_sample_with_replacement_like_reference_capi():  # test_capi.cpp:80-112
+    W = wrs.Weights.generate("powerlaw", 1.5, 200, 11)
+    n, k = 200, 5000
+    items, counts = wrs.sample_with_replacement(W, k, 9, 2)
+    assert items.size <= n and np.all(items < n)
+    assert np.unique(items).size == items.size
+    assert int(counts.sum()) == k
+    items2, counts2 = wrs.sample_with_replacement(W, k, 9, 7)  # workers do not matter
+    assert np.array_equal(items2, items) and np.array_equal(counts2, counts)
+    L = wrs.lib()
+    import ctypes as C
+    m = C.c_uint64()
+    buf_i = np.empty(n, np.uint32)
+    buf_c = np.empty(n, np.uint64)
+    assert L.wrs_sample_with_replacement(None, k, 9, 1, buf_i.ctypes.data, buf_c.ctypes.data,
+                                         C.byref(m)) == 1  # WRS_EINVAL
 
 
 @pytest.mark.parametrize("chunk", [None, 3_000_001])
