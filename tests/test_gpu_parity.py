@@ -326,3 +326,31 @@ def test_double_buffered_rebuild_then_draw_on_other_stream(P):
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref), i
     S.check()
     assert_same_table(S, w, S.jobs, P)
+
+
+def test_weight_validation_like_reference():  # test_weights.cpp:14-21, weights.hpp:32-41
+    for bad, item in ((np.array([], np.float64), None), (np.array([1.0, 0.0]), 1),
+                      (np.array([1.0, -2.0]), 1), (np.array([1.0, np.nan]), 1),
+                      (np.array([np.inf]), 0), (np.array([2.0, 3.0, -np.inf, 1.0]), 2)):
+        with pytest.raises(wrs.WrsError) as e:
+            wrs.Weights.from_array(bad)
+        assert e.value.status == 1, bad
+        if item is None:
+            assert "need at least one item" in e.value.message
+        else:
+            assert f"item {item} is not finite and positive" in e.value.message
+    W = wrs.Weights.from_array(np.array([4.0, 1.0, 2.0, 8.0]))  # test_weights.cpp:23-31
+    assert W.total() == 15.0 and W.count() == 4
+
+
+def test_samples_follow_the_weights(P):  # test_alias.cpp:254-286
+    from tests.stats_util import chi_square
+    W = wrs.Weights.from_array(np.array([3.0, 1, 1, 1]))
+    S = wrs.Sampler.build(W, "psa-exact", 2)
+    counts = np.bincount(S.draw(0xC0FFEE, 400_000, 1), minlength=4)
+    assert chi_square(counts, [0.5, 1 / 6, 1 / 6, 1 / 6])[3]
+    w = P.generate_powerlaw(50, 1.0, 3)
+    S = wrs.Sampler.build(wrs.Weights.from_array(w), "psa-exact", 4)
+    a, b = S.draw(99, 100_001, 4), S.draw(99, 100_001, 4)
+    assert np.array_equal(a, b) and not np.array_equal(a, S.draw(100, 100_001, 4))
+    assert chi_square(np.bincount(a, minlength=50), w / w.sum())[3]
