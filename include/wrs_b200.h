@@ -87,6 +87,13 @@ WRS_API wrs_status wrs_b200_sampler_draw_counts_device(const wrs_sampler* s, uin
                                                        uint32_t* d_items, uint64_t* d_counts,
                                                        uint64_t* d_n_unique, void* stream);
 
+/* implied_masses (verify.hpp:43-54) of the sampler's table into out[0..n)
+ * (host or device) and, if worst is not NULL, max_relative_mass_error
+ * (verify.hpp:92-98) against the weights -- on the device, bit for bit.
+ * wrs_sampler_verify_masses uses the same computation.  n < 2^31. */
+WRS_API wrs_status wrs_b200_sampler_implied_masses(const wrs_sampler* s, double* out,
+                                                   double* worst);
+
 /* Copy a named intermediate of the last build (needs WRS_B200_KEEP_WORKSPACE):
  * "counts" (u64 nl, nh), "heavy" (u32 heavy ids), "light_w", "heavy_w" (f64),
  * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries), "block_totals",

@@ -418,29 +418,19 @@ void draw_counts(const wrs_sampler& s, uint64_t seed, uint64_t k, unsigned worke
     *n_unique = m;
 }
 
-// implied_masses (verify.hpp:43-54): Kahan per item in bucket order, so the
-// result is the reference's bit for bit.  Verification utility, not the hot
-// path; runs over a D2H copy of the table.
-double max_rel_mass_error(const wrs_sampler& s) {
-    std::vector<Bucket> b(s.n);
+// implied_masses (verify.hpp:43-54) and max_relative_mass_error (:92-98) on
+// the device, bit for bit (verify_kernels.cu); d_m may be null.
+double implied_masses(const wrs_sampler& s, double* d_m) {
     s.sync_table();
-    ck(cudaMemcpy(b.data(), s.d_b(), s.n * sizeof(Bucket), cudaMemcpyDeviceToHost), "table D2H");
-    std::vector<double> sum(s.n, 0.0), comp(s.n, 0.0);
-    auto kadd = [&](uint32_t i, double x) {
-        const double y = x - comp[i];
-        const double t = sum[i] + y;
-        comp[i] = (t - sum[i]) - y;
-        sum[i] = t;
-    };
-    for (uint64_t i = 0; i < s.n; ++i) {
-        kadd(b[i].item, b[i].share);
-        kadd(b[i].alias, s.wn - b[i].share);
-    }
-    const double* w = s.weights->host_values();
+    ck(cudaStreamSynchronize(s.stream->s), "sync");
     double worst = 0.0;
-    for (uint64_t i = 0; i < s.n; ++i) worst = std::max(worst, std::abs(sum[i] - w[i]) / w[i]);
+    ck(wrsb::implied_masses_device(s.d_b(), s.n, s.wn, s.weights->d_w, d_m, &worst,
+                                   s.stream->s),
+       "implied masses");
     return worst;
 }
+
+double max_rel_mass_error(const wrs_sampler& s) { return implied_masses(s, nullptr); }
 
 }  // namespace
 
@@ -776,6 +766,24 @@ wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream) {
            "PSA launch");
         ck(cudaEventRecord(s->hi_ev[1], s->hi->s), "event");
         ck(cudaStreamWaitEvent(st, s->hi_ev[1], 0), "wait");
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_implied_masses(const wrs_sampler* s, double* out, double* worst) {
+    if (!s || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        const bool dev = is_device_pointer(out);
+        std::unique_ptr<DevBuf> tmp;
+        double* d_m = out;
+        if (!dev) {
+            tmp = std::make_unique<DevBuf>(s->n * sizeof(double));
+            d_m = static_cast<double*>(tmp->p);
+        }
+        const double wv = implied_masses(*s, d_m);
+        if (!dev) ck(cudaMemcpy(out, d_m, s->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        if (worst) *worst = wv;
         return WRS_OK;
     });
 }

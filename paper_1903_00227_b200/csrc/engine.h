@@ -138,6 +138,12 @@ cudaError_t launch_two_level(const TwoLevelDev& tl, uint64_t seed, uint64_t q_be
                              uint64_t q_end, uint64_t k, uint32_t workers, uint32_t* d_out,
                              cudaStream_t st);
 
+// implied_masses + max_relative_mass_error (verify.hpp:43-54, 92-98) on the
+// device, bit-exact: per-item masses into d_m (may be null), the worst
+// relative error into *worst (host).  Synchronous on st.  n < 2^31.
+cudaError_t implied_masses_device(const Bucket* d_b, uint64_t n, double wn, const double* d_w,
+                                  double* d_m, double* worst, cudaStream_t st);
+
 // generate_uniform on the device (weight_file.hpp:32-38): counter-based, so
 // every element is independent and bit-exact; items [offset, offset + n) of
 // the global vector (a shard's slice).

@@ -66,6 +66,7 @@ SIGNATURES = {
     "wrs_b200_sampler_rebuild_async": (C.c_int, [vp, vp]),
     "wrs_b200_sampler_check": (C.c_int, [vp]),
     "wrs_b200_sampler_double_buffer": (C.c_int, [vp]),
+    "wrs_b200_sampler_implied_masses": (C.c_int, [vp, vp, C.POINTER(f64)]),
     "wrs_b200_sampler_draw_device": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp]),
     "wrs_b200_sampler_stage": (C.c_int, [vp, C.c_char_p, vp, u64, C.POINTER(u64)]),
     "wrs_b200_set_timing": (C.c_int, [C.c_int]),
@@ -290,6 +291,14 @@ class Sampler:
 
     def check(self) -> None:
         _check(lib().wrs_b200_sampler_check(self.h))
+
+    def implied_masses(self) -> tuple[np.ndarray, float]:
+        """(per-item implied masses, max relative error vs the weights),
+        verify.hpp:43-54, 92-98, computed on the device."""
+        out = np.empty(self.size, np.float64)
+        worst = f64()
+        _check(lib().wrs_b200_sampler_implied_masses(self.h, _ptr(out), C.byref(worst)))
+        return out, worst.value
 
     def double_buffer(self) -> None:
         """wrs_b200_sampler_double_buffer: rebuilds write a second table."""

@@ -354,3 +354,20 @@ def test_samples_follow_the_weights(P):  # test_alias.cpp:254-286
     a, b = S.draw(99, 100_001, 4), S.draw(99, 100_001, 4)
     assert np.array_equal(a, b) and not np.array_equal(a, S.draw(100, 100_001, 4))
     assert chi_square(np.bincount(a, minlength=50), w / w.sum())[3]
+
+
+def test_implied_masses_on_device_bit_exact(P):  # verify.hpp:43-54, 92-98
+    rng = np.random.default_rng(12)
+    cases = [np.array([3.0, 1, 1, 1]), np.full(64, 0.5), np.array([1.0, 1e-12]), np.array([7.0])]
+    w = np.ones(100)
+    w[0] = 100.0
+    cases.append(w)  # one heavy aliased by every other bucket (test_alias.cpp:173-193)
+    cases += [P.generate_powerlaw(100_003, 1.0, 2), rng.random(250_000) + 1e-9,
+              np.exp(3.0 * rng.standard_normal(77_777))]
+    for w in cases:
+        for jobs in (0, 1, 7):
+            W, S = build(w, jobs)
+            m, worst = S.implied_masses()
+            ref = P.implied_masses(S.buckets(), S.bucket_mean)
+            assert m.tobytes() == ref.tobytes(), (w.size, jobs)
+            assert worst == P.max_relative_mass_error(ref, w), (w.size, jobs)
