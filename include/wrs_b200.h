@@ -29,8 +29,11 @@ WRS_API uint64_t wrs_b200_default_jobs(uint64_t n);
 WRS_API wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
                                                 wrs_weights** out);
 /* Items [lo, hi) of the global vector wrs_weights_generate(dist, param,
- * n_total, seed) would produce, generated directly on the device (a shard's
- * slice).  Only "uniform" (counter-based) is supported per range. */
+ * n_total, seed) would produce, generated on the device (a shard's slice):
+ * "uniform" is counter-based (only the slice is generated); "powerlaw" deals
+ * all n_total items (its Fisher-Yates is global, resolved in parallel on the
+ * device, generate_kernels.cu) and keeps the slice.  wrs_weights_generate
+ * ("powerlaw") uses the same device deal. */
 WRS_API wrs_status wrs_b200_weights_generate_range(const char* dist, double param,
                                                    uint64_t n_total, uint64_t lo, uint64_t hi,
                                                    uint64_t seed, wrs_weights** out);

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -191,6 +192,43 @@ std::vector<double> powerlaw_host(uint64_t n, double s, uint64_t seed) {
         std::swap(w[i - 1], w[j]);
     }
     return w;
+}
+
+// Power-law weights with the shuffle on the device (generate_kernels.cu):
+// the powers (i+1)^-s with the host's libm pow in parallel threads (bit-equal
+// to the reference's std::pow), then the deal resolved on the GPU.
+std::shared_ptr<WeightsData> powerlaw_device(uint64_t n, double s, uint64_t seed) {
+    if (!(s >= 0.0) || !std::isfinite(s))
+        throw std::invalid_argument("power law exponent must be finite and >= 0");
+    if (n == 0) throw std::invalid_argument("weights: need at least one item");
+    if (n > static_cast<uint64_t>(std::numeric_limits<int>::max())) {
+        const auto w = powerlaw_host(n, s, seed);
+        return weights_from_host(w.data(), n);
+    }
+    std::vector<double> pw(n);
+    const unsigned T = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+            const uint64_t lo = n * t / T, hi = n * (t + 1) / T;
+            for (uint64_t i = lo; i < hi; ++i) pw[i] = std::pow(static_cast<double>(i + 1), -s);
+        });
+    for (auto& x : th) x.join();
+    auto wd = std::make_shared<WeightsData>();
+    wd->device = current_device();
+    wd->n = n;
+    wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
+    wd->d_w = static_cast<double*>(wd->storage->p);
+    {
+        DevBuf tmp(n * sizeof(double));
+        ck(cudaMemcpy(tmp.p, pw.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        Stream st;
+        ck(wrsb::fisher_yates_device(static_cast<const double*>(tmp.p), wd->d_w, n,
+                                     wrsb::rng_key(seed, 0x67656e70u), st.s),
+           "power-law deal");
+    }
+    finalize_weights(*wd, "");
+    return wd;
 }
 
 }  // namespace
@@ -481,8 +519,7 @@ wrs_status wrs_weights_generate(const char* dist, double param, uint64_t n, uint
             return WRS_OK;
         }
         if (d == "powerlaw") {
-            const auto w = powerlaw_host(n, param, seed);
-            *out = new wrs_weights{weights_from_host(w.data(), n)};
+            *out = new wrs_weights{powerlaw_device(n, param, seed)};
             return WRS_OK;
         }
         return fail(WRS_EINVAL, "unknown distribution: " + d);
@@ -669,12 +706,27 @@ wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
 wrs_status wrs_b200_weights_generate_range(const char* dist, double param, uint64_t n_total,
                                            uint64_t lo, uint64_t hi, uint64_t seed,
                                            wrs_weights** out) {
-    (void)param;
     if (!dist || !out) return fail(WRS_EINVAL, "null argument");
     return guarded([&]() -> wrs_status {
-        if (std::string(dist) != "uniform")
-            return fail(WRS_EINVAL, "only \"uniform\" is generated per range on the device");
+        const std::string d = dist;
+        if (d != "uniform" && d != "powerlaw")
+            return fail(WRS_EINVAL, "unknown distribution: " + d);
         if (lo >= hi || hi > n_total) return fail(WRS_EINVAL, "bad range");
+        if (d == "powerlaw") {
+            // the deal is global: generate all n_total, keep [lo, hi)
+            auto full = powerlaw_device(n_total, param, seed);
+            auto wd = std::make_shared<WeightsData>();
+            wd->device = current_device();
+            wd->n = hi - lo;
+            wd->storage = std::make_unique<DevBuf>(wd->n * sizeof(double));
+            wd->d_w = static_cast<double*>(wd->storage->p);
+            ck(cudaMemcpy(wd->d_w, full->d_w + lo, wd->n * sizeof(double),
+                          cudaMemcpyDeviceToDevice),
+               "slice");
+            finalize_weights(*wd, "");
+            *out = new wrs_weights{wd};
+            return WRS_OK;
+        }
         auto wd = std::make_shared<WeightsData>();
         wd->device = current_device();
         wd->n = hi - lo;

@@ -144,6 +144,12 @@ cudaError_t launch_two_level(const TwoLevelDev& tl, uint64_t seed, uint64_t q_be
 cudaError_t implied_masses_device(const Bucket* d_b, uint64_t n, double wn, const double* d_w,
                                   double* d_m, double* worst, cudaStream_t st);
 
+// The power-law generator's Fisher-Yates deal (weight_file.hpp:47-52) on the
+// device, identical to the sequential swaps: d_out = shuffle of d_in with
+// RngStream key `key`.  Synchronous on st.  n < 2^31.
+cudaError_t fisher_yates_device(const double* d_in, double* d_out, uint64_t n, uint64_t key,
+                                cudaStream_t st);
+
 // generate_uniform on the device (weight_file.hpp:32-38): counter-based, so
 // every element is independent and bit-exact; items [offset, offset + n) of
 // the global vector (a shard's slice).

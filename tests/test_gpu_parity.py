@@ -371,3 +371,16 @@ def test_implied_masses_on_device_bit_exact(P):  # verify.hpp:43-54, 92-98
             ref = P.implied_masses(S.buckets(), S.bucket_mean)
             assert m.tobytes() == ref.tobytes(), (w.size, jobs)
             assert worst == P.max_relative_mass_error(ref, w), (w.size, jobs)
+
+
+def test_powerlaw_device_deal_matches_reference_generator(P):  # weight_file.hpp:42-54
+    for n, s_, seed in ((1, 1.0, 3), (2, 1.0, 3), (3, 0.5, 9), (1000, 1.0, 1), (65537, 2.0, 5),
+                        (1_000_003, 0.5, 42), (4_000_000, 1.0, 7)):
+        W = wrs.Weights.generate("powerlaw", s_, n, seed)
+        assert np.array_equal(W.values(), P.generate_powerlaw(n, s_, seed)), (n, s_, seed)
+    # shard slices of the global deal
+    n = 300_007
+    full = P.generate_powerlaw(n, 1.0, 11)
+    for lo, hi in ((0, 1000), (150_000, 300_007), (1, 2)):
+        Wr = wrs.Weights.generate_range("powerlaw", 1.0, n, lo, hi, 11)
+        assert np.array_equal(Wr.values(), full[lo:hi])
