@@ -116,6 +116,38 @@ __global__ void piped(const double* __restrict__ gin, double* out, long long* cy
     *cyc = t1 - t0;
 }
 
+// two independent one-DADD recurrences (hi over X, lo over E) with the
+// per-step states stored to smem: the lane-0 loop of a split carry chain
+__global__ void two_chains(const double* __restrict__ gin, double* out, long long* cyc) {
+    __shared__ double X[N / 4], E[N / 4], H[N / 4], L[N / 4];
+    for (int i = threadIdx.x; i < N / 4; i += 32) {
+        X[i] = gin[i];
+        E[i] = gin[N / 4 + i] * 1e-9;
+    }
+    __syncwarp();
+    if (threadIdx.x) return;
+    double hi = 0, lo = 0;
+    const long long t0 = clock64();
+    for (int k = 0; k < N / 4; k += 8) {
+        double xa[8], ec[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xa[u] = X[k + u];
+            ec[u] = E[k + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            H[k + u] = hi;
+            hi = hi + xa[u];
+            L[k + u] = lo;
+            lo = lo + ec[u];
+        }
+    }
+    const long long t1 = clock64();
+    out[0] = hi + lo + H[7] + L[9];
+    *cyc = (t1 - t0) * 4;  // per pair: cycles x 4 / N
+}
+
 __global__ void dadd_rate(double* out, long long* cyc, int iters) {
     double a[8];
 #pragma unroll
@@ -156,6 +188,7 @@ int main() {
     run("CS4 no value", chain<CS4, false>);
     run("CS2 no value", chain<CS2, false>);
     run("pipelined CompSumPos + value", piped);
+    run("two 1-DADD chains (per pair of adds)", two_chains);
     const int iters = 1 << 14;
     dadd_rate<<<1, 32>>>(out, cyc, iters);
     cudaDeviceSynchronize();
