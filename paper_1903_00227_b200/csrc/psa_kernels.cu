@@ -647,10 +647,16 @@ k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__
 //   stores (scattered 16-B bucket stores here would be half-sector writes,
 //   which the ECC-protected HBM turns into read-modify-writes).
 // ===========================================================================
-constexpr int K4_S = 32;      // steps per phase (= max items consumed per list)
-constexpr int K4_WARPS = 2;
-constexpr int K4_LW = K4_S + 1;   // light window row stride (odd -> no bank conflicts)
-constexpr int K4_HW = K4_S + 2;   // heavy window row stride (S + 1 lookahead)
+// S = 30 and 11 warps per CTA: 644 B of windows per lane, so one CTA of 11
+// warps fills an SM's shared memory (226.7 KB).  At n = 1e8 (97657 jobs =
+// 3052 warps) the 1628 resident warps run the pack in 2 rounds; 32-step
+// phases (672 B per lane) allowed only 10 warps per SM, i.e. 3 rounds, the
+// last one with 6% of the warps.
+constexpr int K4_S = 30;      // steps per phase (= max items consumed per list)
+constexpr int K4_WARPS = 11;
+constexpr int K4_LW = K4_S + 1;     // light window row stride (odd -> no bank conflicts)
+constexpr int K4_HWIN = K4_S + 2;   // heavy window entries (S + 1 lookahead)
+constexpr int K4_HW = K4_S + 3;     // heavy window row stride (odd -> no bank conflicts)
 
 enum : int { ST_MAIN = 0, ST_TAILA = 1, ST_TAILB = 2, ST_DONE = 3 };
 
@@ -745,7 +751,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
         int li = 0, hj = static_cast<int>(j - wh0);
         double cLw = S.lw[lane][0];
         uint32_t hCur = S.hix[lane][0];  // heavy_at(j): slot of min(j, nh-1) = wh0
-        int qn = min(min(hj + 1, hlast), K4_HW - 1);
+        int qn = min(min(hj + 1, hlast), K4_HWIN - 1);
         uint32_t hNext = S.hix[lane][qn];
         double hNextW = S.hw[lane][qn];
 #pragma unroll 2
@@ -783,7 +789,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
             if (lightOp) cLw = S.lw[lane][min(li, K4_S - 1)];
             if (heavyOp) {
                 hCur = hNext;
-                qn = min(min(hj + 1, hlast), K4_HW - 1);
+                qn = min(min(hj + 1, hlast), K4_HWIN - 1);
                 hNext = S.hix[lane][qn];
                 hNextW = S.hw[lane][qn];
             }
