@@ -172,7 +172,8 @@ k_total(const double* __restrict__ w, uint64_t n, int D, double* node_val,
 constexpr int K1_THREADS = 256;
 constexpr int K1_ROWS = 16;
 constexpr int K1_TILE = K1_THREADS * K1_ROWS;  // 4096
-constexpr int K1_SLOTS = K1_ROWS * (K1_THREADS / 32);  // 128 (row, warp) cells
+constexpr int K1_SLOTS = K1_ROWS * (K1_THREADS / 32);  // (row, warp) cells
+constexpr int K1_CPL = K1_SLOTS / 32;                  // cells per lane in the tile scan
 constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62,
                              VAL_MASK = (1ull << 62) - 1;
 
@@ -212,11 +213,11 @@ __device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint
     }
     __syncthreads();
     if (warp == 0) {
-        uint32_t a[4], b[4], sa = 0, sb = 0;
+        uint32_t a[K1_CPL], b[K1_CPL], sa = 0, sb = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            a[q] = __popc(C.lm[lane * 4 + q]);
-            b[q] = __popc(C.hm[lane * 4 + q]);
+        for (int q = 0; q < K1_CPL; ++q) {
+            a[q] = __popc(C.lm[lane * K1_CPL + q]);
+            b[q] = __popc(C.hm[lane * K1_CPL + q]);
             sa += a[q];
             sb += b[q];
         }
@@ -232,9 +233,9 @@ __device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint
         }
         uint32_t ea = ia - sa, eb = ib - sb;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            C.exL[lane * 4 + q] = ea;
-            C.exH[lane * 4 + q] = eb;
+        for (int q = 0; q < K1_CPL; ++q) {
+            C.exL[lane * K1_CPL + q] = ea;
+            C.exH[lane * K1_CPL + q] = eb;
             ea += a[q];
             eb += b[q];
         }
