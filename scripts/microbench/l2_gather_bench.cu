@@ -66,6 +66,51 @@ __global__ void __launch_bounds__(256) k_ldgsts(const uint4* __restrict__ t, con
     }
 }
 
+// texture path: int4 texels through the TEX pipe (tex1Dfetch on a linear buffer)
+template <int U>
+__global__ void __launch_bounds__(256) k_tex(cudaTextureObject_t tex, const uint32_t* __restrict__ idx,
+                                             uint64_t k, uint32_t* __restrict__ out) {
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * (256 * U) + threadIdx.x;
+    uint32_t r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = idx[p0 + u * 256];
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = tex1Dfetch<int4>(tex, static_cast<int>(r[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) out[p0 + u * 256] = static_cast<uint32_t>(v[u].x ^ v[u].w);
+}
+
+// half the rows through LDGSTS, half through the TEX pipe
+template <int U>
+__global__ void __launch_bounds__(256) k_mix_tex(cudaTextureObject_t tex, const uint4* __restrict__ t,
+                                                 const uint32_t* __restrict__ idx, uint64_t k,
+                                                 uint32_t* __restrict__ out) {
+    __shared__ uint4 buf[256 * U];
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * (256 * U * 2) + threadIdx.x;
+    uint32_t r[U], q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        r[u] = idx[p0 + u * 256];
+        q[u] = idx[p0 + (U + u) * 256];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&buf[u * 256 + threadIdx.x]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(t + r[u]));
+    }
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = tex1Dfetch<int4>(tex, static_cast<int>(q[u]));
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint4 a = buf[u * 256 + threadIdx.x];
+        out[p0 + u * 256] = a.x ^ a.w;
+        out[p0 + (U + u) * 256] = static_cast<uint32_t>(v[u].x ^ v[u].w);
+    }
+}
+
 int main() {
     const uint32_t n = 1u << 21;  // 32 MB table
     const uint64_t k = 1ull << 28;
@@ -98,6 +143,18 @@ int main() {
     time("ldg.nc.L1::no_allocate U8", [&] { k_ldg<1, 8><<<k / 2048, 256>>>(t, idx, k, out); });
     time("ldg.cg U8", [&] { k_ldg<2, 8><<<k / 2048, 256>>>(t, idx, k, out); });
     time("ldgsts.cg U8", [&] { k_ldgsts<8><<<k / 2048, 256>>>(t, idx, k, out); });
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = t;
+    rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+    rd.res.linear.sizeInBytes = (size_t)n * 16;
+    cudaTextureDesc td{};
+    td.readMode = cudaReadModeElementType;
+    cudaTextureObject_t tex = 0;
+    printf("tex create: %s\n", cudaGetErrorString(cudaCreateTextureObject(&tex, &rd, &td, nullptr)));
+    time("tex1Dfetch int4 U8", [&] { k_tex<8><<<k / 2048, 256>>>(tex, idx, k, out); });
+    time("tex1Dfetch int4 U16", [&] { k_tex<16><<<k / 4096, 256>>>(tex, idx, k, out); });
+    time("mix ldgsts+tex U4+U4", [&] { k_mix_tex<4><<<k / 2048, 256>>>(tex, t, idx, k, out); });
     time("ldgsts.ca U8", [&] { k_ldgsts<8, true><<<k / 2048, 256>>>(t, idx, k, out); });
     time("ldgsts.cg U4", [&] { k_ldgsts<4><<<k / 1024, 256>>>(t, idx, k, out); });
     time("ldgsts.cg U12", [&] { k_ldgsts<12><<<k / 3072, 256>>>(t, idx, k, out); });
