@@ -445,7 +445,7 @@ def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):
     Wd.free()
     k = args.k
     host_out = torch.empty(k, dtype=torch.int32, pin_memory=True)
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
     times = []
     for i in range(1 + steps):
         torch.cuda.synchronize()

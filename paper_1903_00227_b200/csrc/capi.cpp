@@ -82,11 +82,11 @@ std::atomic<int> g_timing{0};
 struct DevBuf {
     void* p = nullptr;
     DevBuf() = default;
-    explicit DevBuf(size_t bytes) { ck(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
+    explicit DevBuf(size_t bytes) { ck(wrsb::dev_malloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) wrsb::dev_free(p);
     }
 };
 

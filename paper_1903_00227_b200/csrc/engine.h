@@ -10,6 +10,10 @@
 
 namespace wrsb {
 
+// Caching device allocator for the library's large buffers (alloc.cpp).
+cudaError_t dev_malloc(void** p, size_t bytes);
+void dev_free(void* p);
+
 // PSA job count used by algo "psa": one job = one thread's sequential pack
 // chain, so P sets the build's parallelism and the job length its latency.
 // Jobs of J = n / 49152 items rounded down to a power of two, clamped to

@@ -893,7 +893,7 @@ static int k0_depth(uint64_t n) {
 template <typename T>
 static cudaError_t ws_alloc(Workspace& ws, T*& ptr, uint64_t count) {
     const uint64_t by = count * sizeof(T) + 64;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ptr), by);
+    cudaError_t e = dev_malloc(reinterpret_cast<void**>(&ptr), by);
     if (e == cudaSuccess) ws.bytes += by;
     return e;
 }
@@ -957,7 +957,7 @@ void workspace_free(Workspace& ws) {
                     ws.carries,  ws.split_l,  ws.split_h,     ws.split_s,    ws.sc,
                     ws.lalias_own, ws.hshare_own};
     for (void* p : ptrs)
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
     ws = Workspace{};
 }
 

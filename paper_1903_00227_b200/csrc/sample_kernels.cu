@@ -882,13 +882,13 @@ static uint64_t region_bytes(const RegionPlan& p, uint64_t chunk, RegionBuffers*
 cudaError_t SampleWorkspace::reserve(uint64_t need) {
     if (need <= bytes) return cudaSuccess;
     release();
-    cudaError_t e = cudaMalloc(&base, need);
+    cudaError_t e = dev_malloc(&base, need);
     if (e == cudaSuccess) bytes = need;
     return e;
 }
 
 void SampleWorkspace::release() {
-    if (base) cudaFree(base);
+    if (base) dev_free(base);
     base = nullptr;
     bytes = 0;
 }
@@ -972,10 +972,10 @@ cudaError_t CountWorkspace::reserve(uint64_t need) {
     if (need <= n && hits) return cudaSuccess;
     release();
     const uint64_t nt = (need + CC_TILE - 1) / CC_TILE + 1;
-    cudaError_t e = cudaMalloc(&hits, 2 * need * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&count, need * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMalloc(&tile_cnt, nt * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&tile_off, nt * sizeof(uint64_t));
+    cudaError_t e = dev_malloc(reinterpret_cast<void**>(&hits), 2 * need * sizeof(uint32_t));
+    if (e == cudaSuccess) e = dev_malloc(reinterpret_cast<void**>(&count), need * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = dev_malloc(reinterpret_cast<void**>(&tile_cnt), nt * sizeof(uint32_t));
+    if (e == cudaSuccess) e = dev_malloc(reinterpret_cast<void**>(&tile_off), nt * sizeof(uint64_t));
     if (e != cudaSuccess) {
         release();
         return e;
@@ -987,7 +987,7 @@ cudaError_t CountWorkspace::reserve(uint64_t need) {
 void CountWorkspace::release() {
     for (void* p : {static_cast<void*>(hits), static_cast<void*>(count),
                     static_cast<void*>(tile_cnt), static_cast<void*>(tile_off)})
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
     hits = nullptr;
     count = nullptr;
     tile_cnt = nullptr;
