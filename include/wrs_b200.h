@@ -76,6 +76,16 @@ WRS_API wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t s
                                                 uint64_t count, unsigned workers,
                                                 uint32_t* d_out, void* stream);
 
+/* Philox draw mode (north star: counter-based Philox uniforms): draw q of
+ * the call is Philox4x32-10(counter (q_lo, q_hi, 0, 0), key (seed_lo,
+ * seed_hi)) -> words o0..o3; bucket = ((o1:o0) * n) >> 64, coin = ((o3:o2)
+ * >> 11) * 2^-53 * bucket_mean, answer ia[coin >= share] (alias.hpp:265-269).
+ * Not the reference's stream (wrs_sampler_draw is); checked by replaying the
+ * same uniforms on the table.  Device output, asynchronous on `stream`. */
+WRS_API wrs_status wrs_b200_sampler_draw_philox_device(const wrs_sampler* s, uint64_t seed,
+                                                       uint64_t count, uint32_t* d_out,
+                                                       void* stream);
+
 /* Aggregated draws: the distinct items of
  * wrs_sampler_draw(s, seed, k, workers, ...) with their multiplicities,
  * items ascending.  items / counts hold min(k, n) entries; *n_unique gets

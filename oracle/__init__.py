@@ -96,6 +96,8 @@ class Port:
         lib.wo_implied_masses.argtypes = [vp, u64, f64, vp]
         lib.wo_two_level_sample_range.argtypes = [vp, vp, vp, vp, u64, vp, f64, u64, u64,
                                                   C.c_uint32, u64, u64, vp]
+        lib.wo_philox4x32_10.argtypes = [vp, C.c_uint32, C.c_uint32]
+        lib.wo_sample_philox_range.argtypes = [vp, u64, f64, u64, u64, u64, vp]
         lib.wo_max_relative_mass_error.restype = f64
         lib.wo_max_relative_mass_error.argtypes = [vp, vp, u64]
 
@@ -211,6 +213,17 @@ class Port:
     def implied_masses(self, buckets, wn: float) -> np.ndarray:
         out = np.empty(buckets.size, np.float64)
         self.lib.wo_implied_masses(_ptr(buckets), buckets.size, wn, _ptr(out))
+        return out
+
+    def philox4x32_10(self, ctr, key):
+        c = np.array(ctr, np.uint32)
+        self.lib.wo_philox4x32_10(_ptr(c), int(key[0]), int(key[1]))
+        return c
+
+    def sample_philox_range(self, buckets, wn, seed, q_lo, q_hi) -> np.ndarray:
+        out = np.empty(q_hi - q_lo, np.uint32)
+        self.lib.wo_sample_philox_range(_ptr(buckets), buckets.size, wn, seed, q_lo, q_hi,
+                                        _ptr(out))
         return out
 
     def two_level_build(self, w, groups: int):

@@ -486,6 +486,37 @@ void wo_two_level_sample_range(const wo_bucket* const* tables, const uint64_t* s
     }
 }
 
+/* Philox4x32-10: Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as
+ * easy as 1, 2, 3" (SC'11) -- multipliers 0xD2511F53 / 0xCD9E8D57, Weyl key
+ * increments 0x9E3779B9 / 0xBB67AE85, ten rounds. */
+void wo_philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        c[1] = (uint32_t)p1;
+        c[3] = (uint32_t)p0;
+        c[0] = n0;
+        c[2] = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+void wo_sample_philox_range(const wo_bucket* b, uint64_t n, double wn, uint64_t seed,
+                            uint64_t q_lo, uint64_t q_hi, uint32_t* out) {
+    for (uint64_t q = q_lo; q < q_hi; ++q) {
+        uint32_t o[4] = {(uint32_t)q, (uint32_t)(q >> 32), 0u, 0u};
+        wo_philox4x32_10(o, (uint32_t)seed, (uint32_t)(seed >> 32));
+        const uint64_t r = ((uint64_t)o[1] << 32) | o[0];
+        const uint64_t i = (uint64_t)(((unsigned __int128)r * n) >> 64);
+        const uint64_t r2 = ((uint64_t)o[3] << 32) | o[2];
+        const double x = ((double)(r2 >> 11) * 0x1.0p-53) * wn;
+        out[q - q_lo] = x >= b[i].share ? b[i].alias : b[i].item;
+    }
+}
+
 /* -------------------------------------------------------------- verify */
 
 /* kahan_sum: verify.hpp:26-38; implied_masses: verify.hpp:43-54 */

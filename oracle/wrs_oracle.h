@@ -118,6 +118,14 @@ void wo_two_level_sample_range(const wo_bucket* const* tables, const uint64_t* s
                                uint64_t k, uint32_t workers, uint64_t q_lo, uint64_t q_hi,
                                uint32_t* out);
 
+/* Philox4x32-10 (Salmon et al. SC'11, Random123): c[4] in place, key (k0, k1). */
+void wo_philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1);
+/* Philox draw mode replay (include/wrs_b200.h): draws [q_lo, q_hi) of the
+ * table with uniforms from Philox4x32-10(counter q, key seed) through the
+ * reference's ia[x >= share] rule (alias.hpp:265-269). */
+void wo_sample_philox_range(const wo_bucket* b, uint64_t n, double bucket_mean, uint64_t seed,
+                            uint64_t q_lo, uint64_t q_hi, uint32_t* out);
+
 /* implied_masses + max_relative_mass_error (verify.hpp:43-54, 92-98). */
 void wo_implied_masses(const wo_bucket* b, uint64_t n, double bucket_mean, double* m);
 double wo_max_relative_mass_error(const double* m, const double* w, uint64_t n);

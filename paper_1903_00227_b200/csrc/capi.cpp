@@ -338,7 +338,8 @@ std::unique_ptr<wrs_sampler> build_psa(const std::shared_ptr<WeightsData>& wd, u
 // one draw to the next through sws_ev, so draws on different streams never
 // share it concurrently.
 void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, uint64_t k,
-               uint32_t workers, uint32_t base, uint32_t* out, cudaStream_t st) {
+               uint32_t workers, uint32_t base, uint32_t* out, cudaStream_t st,
+               uint64_t stream_id = wrsb::kSampleStream) {
     std::lock_guard<std::mutex> g(s.sws_mu);
     if (!s.sws_ev) {
         ck(cudaEventCreateWithFlags(&s.sws_ev, cudaEventDisableTiming), "event");
@@ -349,7 +350,7 @@ void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, ui
     ck(cudaStreamWaitEvent(s.side->s, s.sws_ev, 0), "wait");
     const int tb = s.front.load();
     if (s.dbuf) ck(cudaStreamWaitEvent(st, s.built_ev[tb], 0), "wait");
-    ck(wrsb::launch_sample(s.table(tb), s.n, s.wn, seed, wrsb::kSampleStream, q0, q1, k, workers,
+    ck(wrsb::launch_sample(s.table(tb), s.n, s.wn, seed, stream_id, q0, q1, k, workers,
                            base, out, st, &s.sws, s.side->s, s.side_ev),
        "K5 launch");
     ck(cudaEventRecord(s.sws_ev, st), "event");
@@ -890,6 +891,17 @@ wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t seed, uin
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
         sample_on(*s, seed, 0, count, count, workers ? workers : 1, 0, d_out, st);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_sampler_draw_philox_device(const wrs_sampler* s, uint64_t seed,
+                                               uint64_t count, uint32_t* d_out, void* stream) {
+    if (!s || (!d_out && count)) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        sample_on(*s, seed, 0, count, count, 1, 0, d_out, st, wrsb::kPhiloxStream);
         return WRS_OK;
     });
 }

@@ -50,6 +50,30 @@ __host__ __device__ __forceinline__ uint64_t rng_derive(uint64_t key, uint64_t s
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// Philox4x32-10 (Salmon et al., SC'11 "Parallel random numbers: as easy as
+// 1, 2, 3"): 10 rounds of two 32x32 multiplies on a 4-word counter with a
+// 2-word key bumped by the Weyl constants.  Used by the optional Philox draw
+// mode (north star), not by the reference-parity draws.
+__host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+    constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#if defined(__CUDACC__)
+#pragma unroll
+#endif
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = static_cast<uint64_t>(M0) * c[0];
+        const uint64_t p1 = static_cast<uint64_t>(M1) * c[2];
+        const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+        const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        k0 += W0;
+        k1 += W1;
+    }
+}
+
 #if defined(__CUDACC__)
 // Neumaier compensated sum, parallel.hpp:70-81 (the isfinite guard keeps an
 // infinite running value from poisoning the low word).  Written branch-free:

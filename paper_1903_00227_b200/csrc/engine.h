@@ -98,6 +98,9 @@ struct SampleWorkspace {
 // the scratch), and st waits for it (side_ev) before the first gather.  A
 // draw issued right behind a rebuild thus scatters while the build runs.
 constexpr uint64_t kSampleStream = 0x616c6961u;
+// stream_id selecting the Philox draw mode (north star: counter-based Philox
+// uniforms): draw q from Philox4x32-10(counter q, key seed), workers ignored.
+constexpr uint64_t kPhiloxStream = ~0ull;
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
                           uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,

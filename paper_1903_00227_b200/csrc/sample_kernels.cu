@@ -47,6 +47,8 @@ struct DrawGeom {
     uint32_t W;         // workers
     uint64_t per, rem, big;  // k/W, k%W, rem*(per+1)
     double inv_p1, inv_p;    // 1/(per+1), 1/per for the division estimate
+    uint32_t philox;         // Philox draw mode (kPhiloxStream): W = 1, key = seed
+    uint32_t pk0, pk1;
 };
 
 DrawGeom make_geom(uint64_t n, double wn, uint64_t seed, uint64_t stream_id, uint64_t k,
@@ -56,6 +58,10 @@ DrawGeom make_geom(uint64_t n, double wn, uint64_t seed, uint64_t stream_id, uin
     g.wn = wn;
     g.base_key = rng_key(seed, stream_id);
     g.k = k;
+    g.philox = stream_id == kPhiloxStream;
+    g.pk0 = static_cast<uint32_t>(seed);
+    g.pk1 = static_cast<uint32_t>(seed >> 32);
+    if (g.philox) W = 1;  // one counter space: draw q uses counter q
     g.W = W ? W : 1;
     g.per = k / g.W;
     g.rem = k % g.W;
@@ -162,6 +168,28 @@ __device__ __forceinline__ double draw_coin(const DrawGeom& g, uint64_t key, uin
     return (static_cast<double>(r >> 11) * 0x1.0p-53) * g.wn;
 }
 
+// Philox draw mode: draw q = Philox4x32-10(counter (q_lo, q_hi, 0, 0), key
+// (seed_lo, seed_hi)) -> words o0..o3; bucket = ((o1:o0) * n) >> 64, coin =
+// ((o3:o2) >> 11) * 2^-53 * bucket_mean, answer ia[coin >= share].
+__device__ __forceinline__ void philox_words(const DrawGeom& g, uint64_t q, uint32_t o[4]) {
+    o[0] = static_cast<uint32_t>(q);
+    o[1] = static_cast<uint32_t>(q >> 32);
+    o[2] = 0;
+    o[3] = 0;
+    philox4x32_10(o, g.pk0, g.pk1);
+}
+__device__ __forceinline__ uint32_t philox_bucket(const DrawGeom& g, uint64_t q) {
+    uint32_t o[4];
+    philox_words(g, q, o);
+    return mulhi_n32((static_cast<uint64_t>(o[1]) << 32) | o[0], static_cast<uint32_t>(g.n));
+}
+__device__ __forceinline__ double philox_coin(const DrawGeom& g, uint64_t q) {
+    uint32_t o[4];
+    philox_words(g, q, o);
+    const uint64_t r = (static_cast<uint64_t>(o[3]) << 32) | o[2];
+    return (static_cast<double>(r >> 11) * 0x1.0p-53) * g.wn;
+}
+
 __device__ __forceinline__ uint4 ld_bucket(const Bucket* b, uint64_t i) {
     uint4 v;
     asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -180,7 +208,7 @@ __device__ __forceinline__ uint32_t pick(const uint4& bk, double x) {
 constexpr int K5_THREADS = 256;
 constexpr int K5_UNROLL = 8;
 
-template <bool W1>
+template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(K5_THREADS)
 k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_end,
          uint32_t out_base, uint32_t* __restrict__ out) {
@@ -199,6 +227,11 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
             bidx[u] = 0;
             x[u] = 0.0;
             if (q < q_end) {
+                if (PHX) {
+                    bidx[u] = philox_bucket(g, q);
+                    x[u] = philox_coin(g, q);
+                    continue;
+                }
                 const uint64_t c1 = cur.ctr1(g, q);
                 bidx[u] = bucket_of_ctr(g, c1);
                 x[u] = coin_of_ctr(g, c1);
@@ -297,7 +330,7 @@ __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg) {
 
 // ORDER = false (aggregated draws): the answers are only counted, never put
 // back in draw order, so the tile slots and the run table are not written.
-template <bool W1, bool ORDER = true>
+template <bool W1, bool ORDER = true, bool PHX = false>
 __global__ void __launch_bounds__(RS_THREADS)
 k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restrict__ overflow,
                  uint2* __restrict__ rec, uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
@@ -321,10 +354,16 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
         uint64_t c1 = rng_derive(rg.g.base_key, 0) +
                       (2 * (rg.q0 + tbase + threadIdx.x) + 1) * kGolden;
         const uint64_t step = 2ull * RS_THREADS * kGolden;
+        if (PHX) {
 #pragma unroll
-        for (int r = 0; r < RS_ROWS; ++r) {
-            bk[r] = mulhi_n32(mix64(c1), n32);
-            c1 += step;
+            for (int r = 0; r < RS_ROWS; ++r)
+                bk[r] = philox_bucket(rg.g, rg.q0 + tbase + r * RS_THREADS + threadIdx.x);
+        } else {
+#pragma unroll
+            for (int r = 0; r < RS_ROWS; ++r) {
+                bk[r] = mulhi_n32(mix64(c1), n32);
+                c1 += step;
+            }
         }
     } else {
         DrawCursor<W1> cur;
@@ -414,7 +453,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
 // contiguous run of 2048 slab positions per CTA, so the resident CTAs of the
 // GPU sweep the table region by region; table loads are marked evict-last,
 // record / result streams evict-first.
-template <bool W1>
+template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(256)
 k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
                 const uint2* __restrict__ rec, uint32_t* __restrict__ res) {
@@ -452,7 +491,8 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         if (p < valid_end) {
             double x;
             if (W1) {
-                x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
+                x = PHX ? philox_coin(rg.g, rg.q0 + r[u].x)
+                                : coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
             } else {
                 uint32_t w;
                 uint64_t m;
@@ -469,7 +509,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 // then picks its answer at the slot RB recorded for it.  If a slab ever
 // overflowed (not expected: ~20 sigma of slack), the tile recomputes its
 // draws directly instead, so the output is correct in every case.
-template <bool W1>
+template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(RS_THREADS)
 k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
                    const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
@@ -484,7 +524,13 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         DrawCursor<W1> cur;
         cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
         for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS) {
-            const uint64_t c1 = cur.ctr1(rg.g, rg.q0 + tbase + e);
+            const uint64_t q = rg.q0 + tbase + e;
+            if (PHX) {
+                out[tbase + e] = pick(ld_bucket(b, philox_bucket(rg.g, q)), philox_coin(rg.g, q)) +
+                                 out_base;
+                continue;
+            }
+            const uint64_t c1 = cur.ctr1(rg.g, q);
             out[tbase + e] = pick(ld_bucket(b, bucket_of_ctr(rg.g, c1)), coin_of_ctr(rg.g, c1)) +
                              out_base;
         }
@@ -545,7 +591,7 @@ __device__ __forceinline__ void count_hit(uint32_t* hits, uint64_t n, uint32_t b
     atomicAdd(hits + (alias ? n + b : b), 1u);
 }
 
-template <bool W1>
+template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(256)
 k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
                const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
@@ -582,7 +628,8 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
         if (p < valid_end) {
             double x;
             if (W1) {
-                x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
+                x = PHX ? philox_coin(rg.g, rg.q0 + r[u].x)
+                                : coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
             } else {
                 uint32_t w;
                 uint64_t m;
@@ -597,7 +644,7 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
 
 // Direct counting of draws [q_begin, q_end): the whole call when the table
 // is L2-resident, or (IF_OVERFLOW) the region chunk whose slabs overflowed.
-template <bool W1, bool IF_OVERFLOW>
+template <bool W1, bool IF_OVERFLOW, bool PHX = false>
 __global__ void __launch_bounds__(K5_THREADS)
 k_count_direct(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_end,
                const unsigned* __restrict__ overflow, uint32_t* __restrict__ hits) {
@@ -607,11 +654,19 @@ k_count_direct(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint6
     DrawCursor<W1> cur;
     cur.init(g, first < q_end ? first : q_begin);
     for (uint64_t q = first; q < q_end; q += stride) {
-        const uint64_t c1 = cur.ctr1(g, q);
-        const uint32_t bi = static_cast<uint32_t>(bucket_of_ctr(g, c1));
+        uint32_t bi;
+        double x;
+        if (PHX) {
+            bi = philox_bucket(g, q);
+            x = philox_coin(g, q);
+        } else {
+            const uint64_t c1 = cur.ctr1(g, q);
+            bi = static_cast<uint32_t>(bucket_of_ctr(g, c1));
+            x = coin_of_ctr(g, c1);
+        }
         const uint4 bk = ld_bucket(b, bi);
         const double share = __hiloint2double(static_cast<int>(bk.y), static_cast<int>(bk.x));
-        count_hit(hits, g.n, bi, coin_of_ctr(g, c1) >= share);
+        count_hit(hits, g.n, bi, x >= share);
     }
 }
 
@@ -905,7 +960,10 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
         uint64_t blocks = (cnt + span - 1) / span;
         const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8 * 64;
         if (blocks > cap) blocks = cap;
-        if (g.W == 1)
+        if (g.philox)
+            k_sample<true, true><<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(
+                d_b, g, q_begin, q_end, base, d_out);
+        else if (g.W == 1)
             k_sample<true><<<static_cast<unsigned>(blocks), K5_THREADS, 0, st>>>(d_b, g, q_begin,
                                                                               q_end, base, d_out);
         else
@@ -927,6 +985,8 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
                          sm_scatter);
     cudaFuncSetAttribute(k_region_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          sm_scatter);
+    cudaFuncSetAttribute(k_region_scatter<true, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
     for (uint64_t c0 = q_begin; c0 < q_end; c0 += chunk) {
         RegionGeom rg = plan.rg;
         rg.q0 = c0;
@@ -941,7 +1001,10 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
         const unsigned tiles = static_cast<unsigned>(rg.ntiles);
         const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
         uint32_t* o = d_out + (c0 - q_begin);
-        if (w1)
+        if (g.philox)
+            k_region_scatter<true, true, true><<<tiles, RS_THREADS, sm_scatter, ss>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+        else if (w1)
             k_region_scatter<true><<<tiles, RS_THREADS, sm_scatter, ss>>>(
                 rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
         else
@@ -951,7 +1014,12 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
             if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
             if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
         }
-        if (w1) {
+        if (g.philox) {
+            k_region_gather<true, true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
+                rg, d_b, B.cursor, B.rec, B.res);
+            k_region_unpermute<true, true><<<tiles, RS_THREADS, 0, st>>>(
+                rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
+        } else if (w1) {
             k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
                 rg, d_b, B.cursor, B.rec, B.res);
             k_region_unpermute<true><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,

@@ -76,6 +76,7 @@ SIGNATURES = {
     "wrs_b200_shard_seed": (u64, [u64, u64]),
     "wrs_b200_sampler_draw_shard_device": (C.c_int, [vp, u64, u64, u64, u64, vp, vp]),
     "wrs_b200_sampler_draw_counts": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, C.POINTER(u64)]),
+    "wrs_b200_sampler_draw_philox_device": (C.c_int, [vp, u64, u64, vp, vp]),
     "wrs_b200_two_level_draw_device": (C.c_int, [vp, vp, vp, vp, u64, vp, f64, u64, u64, u64,
                                                  u64, C.c_uint, vp, vp]),
     "wrs_b200_sampler_ipc_handle": (C.c_int, [vp, vp]),
@@ -312,6 +313,11 @@ class Sampler:
                           stream=None) -> None:
         _check(lib().wrs_b200_sampler_draw_shard_device(self.h, seed, shard, count, base,
                                                         _dev_ptr(out), _stream_ptr(stream, out)))
+
+    def draw_philox_device(self, seed: int, count: int, out, stream=None) -> None:
+        """Philox draw mode (wrs_b200_sampler_draw_philox_device)."""
+        _check(lib().wrs_b200_sampler_draw_philox_device(self.h, seed, count, _dev_ptr(out),
+                                                         _stream_ptr(stream, out)))
 
     def draw_counts(self, seed: int, k: int, workers: int = 1) -> tuple[np.ndarray, np.ndarray]:
         """Distinct items of draw(seed, k, workers) (ascending) and their counts."""

@@ -384,3 +384,18 @@ def test_powerlaw_device_deal_matches_reference_generator(P):  # weight_file.hpp
     for lo, hi in ((0, 1000), (150_000, 300_007), (1, 2)):
         Wr = wrs.Weights.generate_range("powerlaw", 1.0, n, lo, hi, 11)
         assert np.array_equal(Wr.values(), full[lo:hi])
+
+
+def test_philox_mode_replays_on_the_table(P):  # north star: Philox uniforms, replayed
+    import torch
+    for n, k, seed in ((1, 1000, 3), (1000, 200_001, 9), (100_003, 3_000_001, 2**40 + 7),
+                       (8_000_003, 6_000_011, 11)):  # the last one takes the region plan
+        w = P.generate_powerlaw(n, 0.5, 11) if n > 1 else np.array([2.0])
+        W, S = build(w)
+        b = S.buckets()
+        out = torch.empty(k, dtype=torch.int32, device="cuda")
+        S.draw_philox_device(seed, k, out)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        for lo, hi in ((0, min(k, 100_000)), (max(0, k - 50_000), k)):
+            assert np.array_equal(got[lo:hi], P.sample_philox_range(b, S.bucket_mean, seed, lo, hi)), (n, lo)

@@ -202,3 +202,13 @@ def test_golden_two_level(P):  # TwoLevelTable (two_level.hpp:26-81), reference-
         for W in (1, 3):
             got = P.two_level_sample_range(tabs, means, bases, top, tm, 7, 5001, W, 0, 5001)
             assert np.array_equal(got, t[f"G{G}/draws_s7_k5001_W{W}"])
+
+
+def test_philox_known_answers(P):
+    # Random123 kat_vectors for philox4x32-10 (Salmon et al., SC'11)
+    kat = [((0, 0, 0, 0), (0, 0), (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+           ((0xffffffff,) * 4, (0xffffffff, 0xffffffff), (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+           ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344), (0xa4093822, 0x299f31d0),
+            (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1))]
+    for ctr, key, want in kat:
+        assert tuple(int(x) for x in P.philox4x32_10(ctr, key)) == want
