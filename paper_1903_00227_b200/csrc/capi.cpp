@@ -469,7 +469,33 @@ double implied_masses(const wrs_sampler& s, double* d_m) {
     return worst;
 }
 
-double max_rel_mass_error(const wrs_sampler& s) { return implied_masses(s, nullptr); }
+// Tables of 2^31 buckets or more (beyond the device sort's item count): the
+// same Kahan sums on the host over a D2H copy of the table.
+double max_rel_mass_error_host(const wrs_sampler& s) {
+    std::vector<Bucket> b(s.n);
+    s.sync_table();
+    ck(cudaMemcpy(b.data(), s.d_b(), s.n * sizeof(Bucket), cudaMemcpyDeviceToHost), "table D2H");
+    std::vector<double> sum(s.n, 0.0), comp(s.n, 0.0);
+    auto kadd = [&](uint32_t i, double x) {  // kahan_sum::add, verify.hpp:28-33
+        const double y = x - comp[i];
+        const double t = sum[i] + y;
+        comp[i] = (t - sum[i]) - y;
+        sum[i] = t;
+    };
+    for (uint64_t i = 0; i < s.n; ++i) {
+        kadd(b[i].item, b[i].share);
+        kadd(b[i].alias, s.wn - b[i].share);
+    }
+    const double* w = s.weights->host_values();
+    double worst = 0.0;
+    for (uint64_t i = 0; i < s.n; ++i) worst = std::max(worst, std::abs(sum[i] - w[i]) / w[i]);
+    return worst;
+}
+
+double max_rel_mass_error(const wrs_sampler& s) {
+    if (s.n > static_cast<uint64_t>(std::numeric_limits<int>::max())) return max_rel_mass_error_host(s);
+    return implied_masses(s, nullptr);
+}
 
 }  // namespace
 
