@@ -7,7 +7,8 @@
 //                      tree combined by arrival counters.
 //   K1  k_partition    partition_items' stable light/heavy split
 //                      (alias.hpp:48-80): one pass, decoupled look-back,
-//                      emits ids AND gathered weights.
+//                      emits heavy ids and the gathered light / heavy weights
+//                      (light ids stay implicit: K4b recovers them).
 //   K2a k_scan_blocks  prefix_sums pass 1 (parallel.hpp:110-115): Neumaier
 //                      total of every 2048-element block, thread per block,
 //                      warp-transposed through shared memory.
@@ -17,9 +18,12 @@
 //                      writing the exclusive prefix arrays (alias.hpp:82-95).
 //   K3  k_split        psa_split binary searches (alias.hpp:122-149), the
 //                      same probe sequence, one thread per split.
-//   K4  k_pack         psa_pack (alias.hpp:160-209), one lane per job, run in
+//   K4a k_pack         psa_pack (alias.hpp:160-209), one lane per job, run in
 //                      S-step phases over per-lane windows staged by warp-wide
-//                      coalesced async copies; buckets flushed per phase.
+//                      coalesced async copies; list-order outputs flushed per
+//                      phase.
+//   K4b k_assemble     the table in index order (full-line 16-B buckets) from
+//                      the weights and K4a's list-order outputs.
 //
 // No stage needs a host round trip: counts live in DevScalars and every grid
 // is sized from upper bounds.

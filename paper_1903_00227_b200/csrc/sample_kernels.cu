@@ -18,16 +18,18 @@
 //           the direct plan tops out near 6.5 TB/s / 132 B = 50 G draws/s.
 //           The region plan reorders the WORK, not the results: draws are
 //           bucketed by table region (2^21 buckets = 32 MB, L2-resident) with
-//           a stable counting sort, the gathers then sweep the table region by
-//           region so every line is fetched from HBM about once, and a final
-//           pass puts the answers back in output order.  Traffic per draw:
-//           8 B record write + 8 B read + 4 B result write + 4 B read + 4 B
-//           output write, plus 16n B of table per pass.
-//     RA  k_region_count    per-tile region histograms
-//     RS  k_scan_*          exclusive scan of the (region, tile) counts
-//     RB  k_region_scatter  (q, bucket) records in region-major order
-//     RC  k_region_gather   coin flip + bucket gather, region by region
-//     RD  k_region_unpermute out[q] = result[position of q]
+//           a tile-local counting sort into per-region slabs (space claimed by
+//           atomics), the gathers then sweep the table region by region so
+//           every line is fetched from HBM about once, and a final pass puts
+//           the answers back in output order.  Traffic per draw: 8 B record
+//           write + 8 B read + 2 B slot write + 2 B read + 4 B result write +
+//           4 B read + 4 B output write, plus 16n B of table per pass.
+//     RB  k_region_scatter   (q, bucket) records, runs per (tile, region)
+//     RC  k_region_gather    coin flip + bucket gather, region by region
+//     RD  k_region_unpermute out[q] = result at the slot RB gave draw q
+//   Aggregated draws reuse RB and count instead of writing (k_region_count,
+//   k_count_fold, k_compact_*); k_two_level_sample routes two-level draws;
+//   the Philox mode is a compile-time variant of every draw kernel.
 #include <cmath>
 #include <cstdlib>
 
