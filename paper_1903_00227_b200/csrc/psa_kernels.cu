@@ -759,8 +759,32 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
         int qn = min(min(hj + 1, hlast), K4_HWIN - 1);
         uint32_t hNext = S.hix[lane][qn];
         double hNextW = S.hw[lane][qn];
+        // Fast phase: every lane of the warp is in the main loop with more
+        // than K4_S lights and K4_S + 1 heavies (and a next heavy) left, so no
+        // tail loop or last-heavy reset can start within this phase: the step
+        // is the main loop's body alone (alias.hpp:175-189), identical values.
+        const bool fast = __all_sync(0xffffffffu, state == ST_MAIN && lrem == K4_S + 1 &&
+                                                      hrem == K4_S + 2 && hlast == K4_S + 2);
 #pragma unroll 2
-        for (int step = 0; step < K4_S; ++step) {
+        for (int step = 0; fast && step < K4_S; ++step) {
+            const double v = rem.value();
+            const bool gt = v > wn;
+            rem.add((gt ? cLw : hNextW) - wn);
+            if (gt) {  // light bucket {w, {idx, heavy_at(j)}}
+                low_word(S.lw[lane][li]) = hCur;
+                ++li;
+                cLw = S.lw[lane][min(li, K4_S - 1)];
+            } else {   // heavy bucket {clamp(rem), {idx, heavy_at(j+1)}}
+                S.hw[lane][hj] = std_max(0.0, std_min(v, wn));
+                S.hix[lane][hj] = hNext;
+                ++hj;
+                hCur = hNext;
+                hNext = S.hix[lane][hj + 1];
+                hNextW = S.hw[lane][hj + 1];
+            }
+        }
+#pragma unroll 2
+        for (int step = 0; !fast && step < K4_S; ++step) {
             const double v = rem.value();
             const bool gt = v > wn;
             const bool lightsLeft = li < lrem, heaviesLeft = hj < hrem;
