@@ -252,8 +252,9 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
 
 // ===========================================================================
 // region plan
-//   Tiles of RS_TILE consecutive draws; warp w of a tile owns the RS_ROWS*32
-//   consecutive draws starting at w*RS_ROWS*32, in rows of 32.  Inside a tile
+//   Tiles of TT * RS_ROWS consecutive draws (TT = 256, 512 or 1024 threads,
+//   more for more regions, tile_threads_for); thread t computes draws t,
+//   t + TT, ... of its tile.  Inside a tile
 //   the draws are laid out by (region, warp, row, lane); each region's run of
 //   the tile moves to and from global memory as one contiguous block through
 //   shared memory.  Region r owns a fixed slab [r*cap, (r+1)*cap) of the
@@ -272,7 +273,7 @@ struct RegionGeom {
     DrawGeom g;
     uint64_t q0;       // first draw of this chunk
     uint64_t kc;       // draws in this chunk
-    uint64_t ntiles;   // ceil(kc / RS_TILE)
+    uint64_t ntiles;   // ceil(kc / tile)
     uint32_t nreg;     // regions
     int shift;         // region = bucket >> shift
     uint32_t cap;      // records per region slab
@@ -325,41 +326,41 @@ __device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t 
 // written to its slab as one contiguous block.  The tile slot of every draw
 // is recorded (q order) for RD, so the (non-deterministic) order inside a run
 // never needs to be reproduced.
-__host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg) {
+__host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t tile) {
     const size_t head = (2 * static_cast<size_t>(nreg) + 1) * 4;
-    return ((head + 15) & ~size_t(15)) + RS_TILE * sizeof(uint2) + RS_TILE * sizeof(uint16_t);
+    return ((head + 15) & ~size_t(15)) + tile * sizeof(uint2) + tile * sizeof(uint16_t);
 }
 
 // ORDER = false (aggregated draws): the answers are only counted, never put
 // back in draw order, so the tile slots and the run table are not written.
-template <bool W1, bool ORDER = true, bool PHX = false>
-__global__ void __launch_bounds__(RS_THREADS)
+template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS>
+__global__ void __launch_bounds__(TT)
 k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restrict__ overflow,
                  uint2* __restrict__ rec, uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
     extern __shared__ __align__(16) unsigned char rs_smem[];
     uint32_t* loc = reinterpret_cast<uint32_t*>(rs_smem);  // counts, then run starts
     uint32_t* goff = loc + rg.nreg + 1;
     uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((2 * rg.nreg + 1) * 4 + 15) & ~15u));
-    uint16_t* regmap = reinterpret_cast<uint16_t*>(stage + RS_TILE);  // region of each staged slot
+    uint16_t* regmap = reinterpret_cast<uint16_t*>(stage + (TT * RS_ROWS));  // region of each staged slot
     const uint64_t tile = blockIdx.x;
-    const uint64_t tbase = tile * RS_TILE;
+    const uint64_t tbase = tile * (TT * RS_ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i <= rg.nreg; i += RS_THREADS) loc[i] = 0;
+    for (uint32_t i = threadIdx.x; i <= rg.nreg; i += TT) loc[i] = 0;
     __syncthreads();
 
     uint32_t bk[RS_ROWS], rank[RS_ROWS];
-    const uint32_t kc_left = static_cast<uint32_t>(umin64(rg.kc - tbase, RS_TILE));
+    const uint32_t kc_left = static_cast<uint32_t>(umin64(rg.kc - tbase, (TT * RS_ROWS)));
     const uint32_t n32 = static_cast<uint32_t>(rg.g.n);
     if (W1) {
         // single worker: counter of draw q is key + (2q + 1) G, and the rows of
-        // a thread are RS_THREADS draws apart
+        // a thread are TT draws apart
         uint64_t c1 = rng_derive(rg.g.base_key, 0) +
                       (2 * (rg.q0 + tbase + threadIdx.x) + 1) * kGolden;
-        const uint64_t step = 2ull * RS_THREADS * kGolden;
+        const uint64_t step = 2ull * TT * kGolden;
         if (PHX) {
 #pragma unroll
             for (int r = 0; r < RS_ROWS; ++r)
-                bk[r] = philox_bucket(rg.g, rg.q0 + tbase + r * RS_THREADS + threadIdx.x);
+                bk[r] = philox_bucket(rg.g, rg.q0 + tbase + r * TT + threadIdx.x);
         } else {
 #pragma unroll
             for (int r = 0; r < RS_ROWS; ++r) {
@@ -372,7 +373,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
         cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
 #pragma unroll
         for (int r = 0; r < RS_ROWS; ++r) {
-            const uint32_t e = r * RS_THREADS + threadIdx.x;
+            const uint32_t e = r * TT + threadIdx.x;
             bk[r] = e < kc_left
                         ? static_cast<uint32_t>(bucket_of_ctr(rg.g, cur.ctr1(rg.g, rg.q0 + tbase + e)))
                         : 0u;
@@ -380,7 +381,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     }
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
-        const uint32_t e = r * RS_THREADS + threadIdx.x;
+        const uint32_t e = r * TT + threadIdx.x;
         rank[r] = 0;
         if (e < kc_left) rank[r] = atomicAdd(&loc[bk[r] >> rg.shift], 1u);
     }
@@ -405,7 +406,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     const uint32_t t32 = static_cast<uint32_t>(tbase);
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
-        const uint32_t e = r * RS_THREADS + threadIdx.x;
+        const uint32_t e = r * TT + threadIdx.x;
         if (e < kc_left) {
             const uint32_t reg = bk[r] >> rg.shift;
             const uint32_t slot = loc[reg] + rank[r];
@@ -415,7 +416,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
         }
     }
     // claim slab space for each non-empty run of this tile
-    for (uint32_t reg = threadIdx.x; reg < rg.nreg; reg += RS_THREADS) {
+    for (uint32_t reg = threadIdx.x; reg < rg.nreg; reg += TT) {
         const uint32_t c = loc[reg + 1] - loc[reg];
         uint32_t g = 0;
         if (c) {
@@ -441,7 +442,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     const uint64_t pol = policy_evict_first();
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
-        const uint32_t i = r * RS_THREADS + threadIdx.x;
+        const uint32_t i = r * TT + threadIdx.x;
         if (i < kc_left) {
             const uint2 v = stage[i];
             uint2* dst = rec + (goff[regmap[i]] + i);
@@ -511,21 +512,21 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 // then picks its answer at the slot RB recorded for it.  If a slab ever
 // overflowed (not expected: ~20 sigma of slack), the tile recomputes its
 // draws directly instead, so the output is correct in every case.
-template <bool W1, bool PHX = false>
-__global__ void __launch_bounds__(RS_THREADS)
+template <bool W1, bool PHX = false, int TT = RS_THREADS>
+__global__ void __launch_bounds__(TT)
 k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
                    const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
                    const uint16_t* __restrict__ slot_of, const uint32_t* __restrict__ res,
                    uint32_t out_base, uint32_t* __restrict__ out) {
-    __shared__ uint32_t stage[RS_TILE];
+    extern __shared__ __align__(16) uint32_t stage[];  // (TT * RS_ROWS) results
     const uint64_t tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t tbase = tile * RS_TILE;
-    const uint32_t tcount = static_cast<uint32_t>(umin64(RS_TILE, rg.kc - tbase));
+    const uint64_t tbase = tile * (TT * RS_ROWS);
+    const uint32_t tcount = static_cast<uint32_t>(umin64((TT * RS_ROWS), rg.kc - tbase));
     if (*overflow) {
         DrawCursor<W1> cur;
         cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
-        for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS) {
+        for (uint32_t e = threadIdx.x; e < tcount; e += TT) {
             const uint64_t q = rg.q0 + tbase + e;
             if (PHX) {
                 out[tbase + e] = pick(ld_bucket(b, philox_bucket(rg.g, q)), philox_coin(rg.g, q)) +
@@ -542,17 +543,17 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
     // full tiles with a 16-B aligned output: each thread owns 4 consecutive
     // draws per pass (one 8-B slot vector, one 16-B output store); the slot
     // vectors are loaded first so they are in flight during the staging
-    constexpr int VP = RS_TILE / (RS_THREADS * 4);  // passes of 4 draws
-    const bool vec = tcount == RS_TILE && (reinterpret_cast<uintptr_t>(out + tbase) & 15) == 0;
+    constexpr int VP = (TT * RS_ROWS) / (TT * 4);  // passes of 4 draws
+    const bool vec = tcount == (TT * RS_ROWS) && (reinterpret_cast<uintptr_t>(out + tbase) & 15) == 0;
     uint2 sv[VP];
     if (vec) {
 #pragma unroll
         for (int i = 0; i < VP; ++i)
-            sv[i] = *reinterpret_cast<const uint2*>(slot_of + tbase + (i * RS_THREADS + threadIdx.x) * 4);
+            sv[i] = *reinterpret_cast<const uint2*>(slot_of + tbase + (i * TT + threadIdx.x) * 4);
     }
     // this tile's runs -> shared memory with LDGSTS: no register staging, so
     // every element of the tile is in flight at once
-    for (uint32_t reg = warp; reg < rg.nreg; reg += RS_WARPS) {
+    for (uint32_t reg = warp; reg < rg.nreg; reg += (TT / 32)) {
         const RunInfo ri = tr[reg];
         const uint32_t l1 = reg + 1 < rg.nreg ? tr[reg + 1].loc : tcount;
         for (uint32_t t = lane; t < l1 - ri.loc; t += 32) cp_async4(&stage[ri.loc + t], res + ri.goff + t);
@@ -563,7 +564,7 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
     if (vec) {
 #pragma unroll
         for (int i = 0; i < VP; ++i) {
-            const uint32_t e0 = (i * RS_THREADS + threadIdx.x) * 4;
+            const uint32_t e0 = (i * TT + threadIdx.x) * 4;
             uint4 o;
             o.x = stage[sv[i].x & 0xffffu] + out_base;
             o.y = stage[sv[i].x >> 16] + out_base;
@@ -572,7 +573,7 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
             *reinterpret_cast<uint4*>(out + tbase + e0) = o;
         }
     } else {
-        for (uint32_t e = threadIdx.x; e < tcount; e += RS_THREADS)
+        for (uint32_t e = threadIdx.x; e < tcount; e += TT)
             out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
     }
 }
@@ -875,7 +876,20 @@ bool use_region_plan(uint64_t n, uint64_t k) {
 struct RegionPlan {
     RegionGeom rg;
     uint64_t rec_slots;  // nreg * cap + ov_cap
+    int tt;              // threads of a scatter / unpermute CTA (tile = tt * RS_ROWS draws)
+    uint32_t tile;
 };
+
+// Tile size by region count: a tile's runs (one per region) should average
+// tens of draws, or the slab writes and the unpermute's run reads fragment
+// (measured at n = 2^30, 512 regions: 8 draws per run with 4096-draw tiles).
+static int tile_threads_for(uint32_t nreg) {
+    if (const char* env = getenv("WRS_B200_TILE_THREADS")) {  // tests: force a tile size
+        const int t = atoi(env);
+        if (t == 256 || t == 512 || t == 1024) return t;
+    }
+    return nreg <= 160 ? 256 : nreg <= 320 ? 512 : 1024;
+}
 
 static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     RegionPlan p{};
@@ -885,11 +899,13 @@ static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     // expected draws per full region + ~20 sigma + a tile of slack
     const double mu = static_cast<double>(chunk) *
                       (static_cast<double>(1ull << p.rg.shift) / static_cast<double>(g.n));
-    const double cap = mu + 20.0 * std::sqrt(mu) + 2.0 * RS_TILE;
+    p.tt = tile_threads_for(p.rg.nreg);
+    p.tile = static_cast<uint32_t>(p.tt * RS_ROWS);
+    const double cap = mu + 20.0 * std::sqrt(mu) + 2.0 * p.tile;
     // slabs are whole multiples of the gather CTA's 2048 positions
     auto round2k = [](uint64_t x) { return static_cast<uint32_t>((x + 2047) & ~uint64_t(2047)); };
-    p.rg.cap = round2k(static_cast<uint64_t>(cap < static_cast<double>(chunk) ? cap : chunk) + RS_TILE);
-    p.rg.ov_cap = round2k(chunk / 64 + 8 * RS_TILE);
+    p.rg.cap = round2k(static_cast<uint64_t>(cap < static_cast<double>(chunk) ? cap : chunk) + p.tile);
+    p.rg.ov_cap = round2k(chunk / 64 + 8 * p.tile);
     p.rec_slots = static_cast<uint64_t>(p.rg.nreg) * p.rg.cap + p.rg.ov_cap;
     return p;
 }
@@ -913,7 +929,7 @@ struct RegionBuffers {
 };
 
 static uint64_t region_bytes(const RegionPlan& p, uint64_t chunk, RegionBuffers* b, void* base) {
-    const uint64_t ntiles = (chunk + RS_TILE - 1) / RS_TILE;
+    const uint64_t ntiles = (chunk + p.tile - 1) / p.tile;
     uint64_t off = 0;
     auto take = [&](uint64_t bytes) {
         const uint64_t o = off;
@@ -950,6 +966,66 @@ void SampleWorkspace::release() {
     bytes = 0;
 }
 
+// One chunk of the region plan with TT-thread tiles: RB (on the side stream
+// when asked), then RC and RD on st.
+template <int TT>
+static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, const DrawGeom& g,
+                               const Bucket* d_b, const RegionBuffers& B, uint32_t base,
+                               uint32_t* o, cudaStream_t st, bool on_side, cudaStream_t side,
+                               cudaEvent_t side_ev) {
+    const int sm_scatter = static_cast<int>(scatter_smem_bytes(rg.nreg, plan.tile));
+    const int sm_unperm = static_cast<int>(plan.tile * sizeof(uint32_t));
+    const bool w1 = g.W == 1;
+    cudaStream_t ss = on_side ? side : st;
+    cudaError_t e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, ss);
+    if (e != cudaSuccess) return e;
+    const unsigned tiles = static_cast<unsigned>(rg.ntiles);
+    const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
+    if (g.philox) {
+        cudaFuncSetAttribute(k_region_scatter<true, true, true, TT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+        k_region_scatter<true, true, true, TT><<<tiles, TT, sm_scatter, ss>>>(
+            rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+    } else if (w1) {
+        cudaFuncSetAttribute(k_region_scatter<true, true, false, TT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+        k_region_scatter<true, true, false, TT><<<tiles, TT, sm_scatter, ss>>>(
+            rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+    } else {
+        cudaFuncSetAttribute(k_region_scatter<false, true, false, TT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+        k_region_scatter<false, true, false, TT><<<tiles, TT, sm_scatter, ss>>>(
+            rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+    }
+    if (on_side) {
+        if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
+    }
+    if (g.philox) {
+        cudaFuncSetAttribute(k_region_unpermute<true, true, TT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
+        k_region_gather<true, true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
+            rg, d_b, B.cursor, B.rec, B.res);
+        k_region_unpermute<true, true, TT><<<tiles, TT, sm_unperm, st>>>(
+            rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
+    } else if (w1) {
+        cudaFuncSetAttribute(k_region_unpermute<true, false, TT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
+        k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
+            rg, d_b, B.cursor, B.rec, B.res);
+        k_region_unpermute<true, false, TT><<<tiles, TT, sm_unperm, st>>>(
+            rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
+    } else {
+        cudaFuncSetAttribute(k_region_unpermute<false, false, TT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
+        k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
+            rg, d_b, B.cursor, B.rec, B.res);
+        k_region_unpermute<false, false, TT><<<tiles, TT, sm_unperm, st>>>(
+            rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
                           uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,
@@ -981,61 +1057,51 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
     RegionBuffers B;
     region_bytes(plan, chunk, &B, ws->base);
     ws->overflow = B.overflow;
-    const int sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg));
-    const bool w1 = g.W == 1;
-    cudaFuncSetAttribute(k_region_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         sm_scatter);
-    cudaFuncSetAttribute(k_region_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         sm_scatter);
-    cudaFuncSetAttribute(k_region_scatter<true, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
     for (uint64_t c0 = q_begin; c0 < q_end; c0 += chunk) {
         RegionGeom rg = plan.rg;
         rg.q0 = c0;
         rg.kc = (q_end - c0) < chunk ? (q_end - c0) : chunk;
-        rg.ntiles = (rg.kc + RS_TILE - 1) / RS_TILE;
+        rg.ntiles = (rg.kc + plan.tile - 1) / plan.tile;
         // first chunk's scatter on the side stream (if any): it does not read
         // the table; later chunks reuse the scratch behind RD on st
         const bool on_side = side && side_ev && c0 == q_begin;
-        cudaStream_t ss = on_side ? side : st;
-        e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, ss);
-        if (e != cudaSuccess) return e;
-        const unsigned tiles = static_cast<unsigned>(rg.ntiles);
-        const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
         uint32_t* o = d_out + (c0 - q_begin);
-        if (g.philox)
-            k_region_scatter<true, true, true><<<tiles, RS_THREADS, sm_scatter, ss>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-        else if (w1)
-            k_region_scatter<true><<<tiles, RS_THREADS, sm_scatter, ss>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-        else
-            k_region_scatter<false><<<tiles, RS_THREADS, sm_scatter, ss>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-        if (on_side) {
-            if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
-            if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
+        switch (plan.tt) {
+            case 256: e = region_pass<256>(plan, rg, g, d_b, B, base, o, st, on_side, side, side_ev); break;
+            case 512: e = region_pass<512>(plan, rg, g, d_b, B, base, o, st, on_side, side, side_ev); break;
+            default: e = region_pass<1024>(plan, rg, g, d_b, B, base, o, st, on_side, side, side_ev); break;
         }
-        if (g.philox) {
-            k_region_gather<true, true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-                rg, d_b, B.cursor, B.rec, B.res);
-            k_region_unpermute<true, true><<<tiles, RS_THREADS, 0, st>>>(
-                rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
-        } else if (w1) {
-            k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-                rg, d_b, B.cursor, B.rec, B.res);
-            k_region_unpermute<true><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,
-                                                                   B.slot_of, B.res, base, o);
-        } else {
-            k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-                rg, d_b, B.cursor, B.rec, B.res);
-            k_region_unpermute<false><<<tiles, RS_THREADS, 0, st>>>(rg, d_b, B.overflow, B.runs,
-                                                                    B.slot_of, B.res, base, o);
-        }
-        e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+// RB for aggregated draws (no slots / run table) at the plan's tile size.
+template <bool W1>
+static cudaError_t count_scatter(int tt, const RegionGeom& rg, const RegionBuffers& B,
+                                 int sm_scatter, cudaStream_t st) {
+    const unsigned tiles = static_cast<unsigned>(rg.ntiles);
+    switch (tt) {
+        case 256:
+            cudaFuncSetAttribute(k_region_scatter<W1, false, false, 256>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+            k_region_scatter<W1, false, false, 256><<<tiles, 256, sm_scatter, st>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+            break;
+        case 512:
+            cudaFuncSetAttribute(k_region_scatter<W1, false, false, 512>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+            k_region_scatter<W1, false, false, 512><<<tiles, 512, sm_scatter, st>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+            break;
+        default:
+            cudaFuncSetAttribute(k_region_scatter<W1, false, false, 1024>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+            k_region_scatter<W1, false, false, 1024><<<tiles, 1024, sm_scatter, st>>>(
+                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+            break;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t CountWorkspace::reserve(uint64_t need) {
@@ -1088,11 +1154,7 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
         if ((e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr))) != cudaSuccess) return e;
         region_bytes(plan, chunk, &B, ws->base);
         ws->overflow = B.overflow;
-        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg));
-        cudaFuncSetAttribute(k_region_scatter<true, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-        cudaFuncSetAttribute(k_region_scatter<false, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
+        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg, plan.tile));
     }
     const unsigned fold_blocks = static_cast<unsigned>(
         umin64((n + 255) / 256, static_cast<uint64_t>(sm_count()) * 8));
@@ -1102,23 +1164,20 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
             RegionGeom rg = plan.rg;
             rg.q0 = c0;
             rg.kc = c1 - c0;
-            rg.ntiles = (rg.kc + RS_TILE - 1) / RS_TILE;
+            rg.ntiles = (rg.kc + plan.tile - 1) / plan.tile;
             if ((e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st)) != cudaSuccess) return e;
-            const unsigned tiles = static_cast<unsigned>(rg.ntiles);
             const unsigned gblocks = static_cast<unsigned>((plan.rec_slots + 2047) / 2048);
             const uint64_t span = static_cast<uint64_t>(K5_THREADS);
             const unsigned dblocks = static_cast<unsigned>(
                 umin64((rg.kc + span - 1) / span, static_cast<uint64_t>(sm_count()) * 8));
             if (w1) {
-                k_region_scatter<true, false><<<tiles, RS_THREADS, sm_scatter, st>>>(
-                    rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+                if ((e = count_scatter<true>(plan.tt, rg, B, sm_scatter, st)) != cudaSuccess) return e;
                 k_region_count<true><<<gblocks, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, B.rec,
                                                               cw->hits);
                 k_count_direct<true, true><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1, B.overflow,
                                                                            cw->hits);
             } else {
-                k_region_scatter<false, false><<<tiles, RS_THREADS, sm_scatter, st>>>(
-                    rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+                if ((e = count_scatter<false>(plan.tt, rg, B, sm_scatter, st)) != cudaSuccess) return e;
                 k_region_count<false><<<gblocks, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, B.rec,
                                                                cw->hits);
                 k_count_direct<false, true><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1,

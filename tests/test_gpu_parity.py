@@ -399,3 +399,27 @@ def test_philox_mode_replays_on_the_table(P):  # north star: Philox uniforms, re
         got = out.cpu().numpy().view(np.uint32)
         for lo, hi in ((0, min(k, 100_000)), (max(0, k - 50_000), k)):
             assert np.array_equal(got[lo:hi], P.sample_philox_range(b, S.bucket_mean, seed, lo, hi)), (n, lo)
+
+
+@pytest.mark.parametrize("tt", [512, 1024])
+def test_region_plan_larger_tiles_bit_exact(P, tt, monkeypatch):
+    """Tables with many regions use 8192- / 16384-draw tiles (forced here on a
+    4-region table, with a chunk that splits the draws, so the bigger tiles'
+    scatter, run table and unpermute are checked end to end)."""
+    import torch
+    monkeypatch.setenv("WRS_B200_TILE_THREADS", str(tt))
+    n = 8_000_003
+    w = P.generate_powerlaw(n, 0.5, 13)
+    W, S = build(w)
+    b = S.buckets()
+    for k, Wk, chunk in ((6_000_011, 1, None), (7_000_000, 3, 2_500_001)):
+        if chunk:
+            monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
+        out = torch.empty(k, dtype=torch.int32, device="cuda")
+        S.draw_device(31, k, Wk, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32),
+                              P.sample_many(b, S.bucket_mean, 31, k, Wk)), (tt, k, Wk)
+        items, counts = S.draw_counts(31, k, Wk)
+        ri, rc = np.unique(P.sample_many(b, S.bucket_mean, 31, k, Wk), return_counts=True)
+        assert np.array_equal(items, ri) and np.array_equal(counts, rc)
