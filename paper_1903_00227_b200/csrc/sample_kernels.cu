@@ -869,8 +869,14 @@ static int region_shift() { return 21; }  // 2^21 buckets = 32 MB per region
 
 bool use_region_plan(uint64_t n, uint64_t k) {
     const uint64_t nreg = (n + (1ull << region_shift()) - 1) >> region_shift();
-    // table well beyond L2 and enough draws per bucket to reuse the lines
-    return n * sizeof(Bucket) > (96ull << 20) && k * 8 >= n && nreg <= RS_MAX_REGIONS;
+    if (const char* env = getenv("WRS_B200_PLAN")) {  // experiments: force a plan
+        if (env[0] == 'd') return false;
+        if (env[0] == 'r') return nreg <= RS_MAX_REGIONS;
+    }
+    // table beyond ~136 MB (measured crossover on B200, scripts/plan_crossover.py:
+    // direct 8.9 vs region 9.5 ms per 1e9 draws at 128 MB, 11.1 vs 9.4 at 160 MB)
+    // and enough draws per bucket to reuse the lines
+    return n * sizeof(Bucket) > (136ull << 20) && k * 8 >= n && nreg <= RS_MAX_REGIONS;
 }
 
 struct RegionPlan {

@@ -90,7 +90,7 @@ def test_counts_region_plan_match_device_draws(P, chunk, monkeypatch):
     import torch
     if chunk:
         monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
-    n = 8_000_003
+    n = 9_500_003
     w = P.generate_powerlaw(n, 0.5, 11)
     W = wrs.Weights.from_array(w)
     S = wrs.Sampler.build(W, "psa", 1)

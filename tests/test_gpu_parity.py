@@ -293,7 +293,7 @@ def test_region_plan_draws_bit_exact(P, chunk, monkeypatch):
     import torch
     if chunk:
         monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
-    n = 8_000_003  # 128 MB table: region plan
+    n = 9_500_003  # 152 MB table: region plan
     w = P.generate_powerlaw(n, 0.5, 11)
     W, S = build(w)
     b = S.buckets()
@@ -389,7 +389,7 @@ def test_powerlaw_device_deal_matches_reference_generator(P):  # weight_file.hpp
 def test_philox_mode_replays_on_the_table(P):  # north star: Philox uniforms, replayed
     import torch
     for n, k, seed in ((1, 1000, 3), (1000, 200_001, 9), (100_003, 3_000_001, 2**40 + 7),
-                       (8_000_003, 6_000_011, 11)):  # the last one takes the region plan
+                       (9_500_003, 6_000_011, 11)):  # the last one takes the region plan
         w = P.generate_powerlaw(n, 0.5, 11) if n > 1 else np.array([2.0])
         W, S = build(w)
         b = S.buckets()
@@ -408,7 +408,7 @@ def test_region_plan_larger_tiles_bit_exact(P, tt, monkeypatch):
     scatter, run table and unpermute are checked end to end)."""
     import torch
     monkeypatch.setenv("WRS_B200_TILE_THREADS", str(tt))
-    n = 8_000_003
+    n = 9_500_003
     w = P.generate_powerlaw(n, 0.5, 13)
     W, S = build(w)
     b = S.buckets()
