@@ -79,7 +79,11 @@ def main():
                 "build_ms": build_ms, "build_gitems_per_s": n / build_ms / 1e6,
                 "build_hbm_frac": BUILD_B * n / (build_ms * 1e-3) / 1e9 / hbm,
                 "draw_ms": draw_ms, "draw_gsamples_per_s": args.draws / draw_ms / 1e6,
-                "draw_hbm_frac": DRAW_B * args.draws / (draw_ms * 1e-3) / 1e9 / hbm,
+                # an L2-resident table's gathers never reach HBM;
+                # its HBM bytes are the 4-B index stores
+                "draw_bytes_per_sample": 4 if 16 * n <= l2 else DRAW_B,
+                "draw_hbm_frac": (4 if 16 * n <= l2 else DRAW_B) * args.draws /
+                                 (draw_ms * 1e-3) / 1e9 / hbm,
                 "generate_s": gen_s,
             }
             rows.append(row)
@@ -93,13 +97,14 @@ def main():
     with open(args.out + ".json", "w") as f:
         json.dump(res, f, indent=1)
     with open(args.out + ".md", "w") as f:
-        f.write("| n | dist | table | L2-resident | build ms | G items/s | build frac | "
-                "draw ms (1e9) | G samples/s | draw frac |\n|---|---|---|---|---|---|---|---|---|---|\n")
+        f.write("| n | dist | table | L2-resident | build ms | G items/s | build frac (72 B/item) | "
+                "draw ms (1e9) | G samples/s | draw frac (B/sample) |\n"
+                "|---|---|---|---|---|---|---|---|---|---|\n")
         for r in rows:
-            f.write("| 2^%d | %s | %.1f MB | %s | %.3f | %.2f | %.2f | %.2f | %.1f | %.2f |\n" % (
+            f.write("| 2^%d | %s | %.1f MB | %s | %.3f | %.2f | %.2f | %.2f | %.1f | %.2f (%d) |\n" % (
                 r["log2_n"], r["dist"], r["table_bytes"] / 2**20, "yes" if r["l2_resident"] else "no",
                 r["build_ms"], r["build_gitems_per_s"], r["build_hbm_frac"], r["draw_ms"],
-                r["draw_gsamples_per_s"], r["draw_hbm_frac"]))
+                r["draw_gsamples_per_s"], r["draw_hbm_frac"], r["draw_bytes_per_sample"]))
 
 
 if __name__ == "__main__":
