@@ -47,10 +47,9 @@ struct DrawGeom {
     uint64_t base_key;  // RngStream(seed, stream).key
     uint64_t k;         // total draws of the call (defines worker slices)
     uint32_t W;         // workers
+    uint32_t philox;    // Philox draw mode (kPhiloxStream): W = 1, base_key = the raw seed
     uint64_t per, rem, big;  // k/W, k%W, rem*(per+1)
     double inv_p1, inv_p;    // 1/(per+1), 1/per for the division estimate
-    uint32_t philox;         // Philox draw mode (kPhiloxStream): W = 1, key = seed
-    uint32_t pk0, pk1;
 };
 
 DrawGeom make_geom(uint64_t n, double wn, uint64_t seed, uint64_t stream_id, uint64_t k,
@@ -58,11 +57,9 @@ DrawGeom make_geom(uint64_t n, double wn, uint64_t seed, uint64_t stream_id, uin
     DrawGeom g{};
     g.n = n;
     g.wn = wn;
-    g.base_key = rng_key(seed, stream_id);
-    g.k = k;
     g.philox = stream_id == kPhiloxStream;
-    g.pk0 = static_cast<uint32_t>(seed);
-    g.pk1 = static_cast<uint32_t>(seed >> 32);
+    g.base_key = g.philox ? seed : rng_key(seed, stream_id);  // Philox keys on the raw seed
+    g.k = k;
     if (g.philox) W = 1;  // one counter space: draw q uses counter q
     g.W = W ? W : 1;
     g.per = k / g.W;
@@ -178,7 +175,7 @@ __device__ __forceinline__ void philox_words(const DrawGeom& g, uint64_t q, uint
     o[1] = static_cast<uint32_t>(q >> 32);
     o[2] = 0;
     o[3] = 0;
-    philox4x32_10(o, g.pk0, g.pk1);
+    philox4x32_10(o, static_cast<uint32_t>(g.base_key), static_cast<uint32_t>(g.base_key >> 32));
 }
 __device__ __forceinline__ uint32_t philox_bucket(const DrawGeom& g, uint64_t q) {
     uint32_t o[4];
@@ -229,7 +226,7 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
             bidx[u] = 0;
             x[u] = 0.0;
             if (q < q_end) {
-                if (PHX) {
+                if constexpr (PHX) {
                     bidx[u] = philox_bucket(g, q);
                     x[u] = philox_coin(g, q);
                     continue;
@@ -357,7 +354,7 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
         uint64_t c1 = rng_derive(rg.g.base_key, 0) +
                       (2 * (rg.q0 + tbase + threadIdx.x) + 1) * kGolden;
         const uint64_t step = 2ull * TT * kGolden;
-        if (PHX) {
+        if constexpr (PHX) {
 #pragma unroll
             for (int r = 0; r < RS_ROWS; ++r)
                 bk[r] = philox_bucket(rg.g, rg.q0 + tbase + r * TT + threadIdx.x);
@@ -494,8 +491,10 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         if (p < valid_end) {
             double x;
             if (W1) {
-                x = PHX ? philox_coin(rg.g, rg.q0 + r[u].x)
-                                : coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
+                if constexpr (PHX)
+                    x = philox_coin(rg.g, rg.q0 + r[u].x);
+                else
+                    x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
             } else {
                 uint32_t w;
                 uint64_t m;
@@ -528,7 +527,7 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
         for (uint32_t e = threadIdx.x; e < tcount; e += TT) {
             const uint64_t q = rg.q0 + tbase + e;
-            if (PHX) {
+            if constexpr (PHX) {
                 out[tbase + e] = pick(ld_bucket(b, philox_bucket(rg.g, q)), philox_coin(rg.g, q)) +
                                  out_base;
                 continue;
@@ -631,8 +630,10 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
         if (p < valid_end) {
             double x;
             if (W1) {
-                x = PHX ? philox_coin(rg.g, rg.q0 + r[u].x)
-                                : coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
+                if constexpr (PHX)
+                    x = philox_coin(rg.g, rg.q0 + r[u].x);
+                else
+                    x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
             } else {
                 uint32_t w;
                 uint64_t m;
@@ -659,7 +660,7 @@ k_count_direct(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint6
     for (uint64_t q = first; q < q_end; q += stride) {
         uint32_t bi;
         double x;
-        if (PHX) {
+        if constexpr (PHX) {
             bi = philox_bucket(g, q);
             x = philox_coin(g, q);
         } else {
