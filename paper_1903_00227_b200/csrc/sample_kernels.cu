@@ -551,11 +551,26 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
             sv[i] = *reinterpret_cast<const uint2*>(slot_of + tbase + (i * TT + threadIdx.x) * 4);
     }
     // this tile's runs -> shared memory with LDGSTS: no register staging, so
-    // every element of the tile is in flight at once
-    for (uint32_t reg = warp; reg < rg.nreg; reg += (TT / 32)) {
-        const RunInfo ri = tr[reg];
-        const uint32_t l1 = reg + 1 < rg.nreg ? tr[reg + 1].loc : tcount;
-        for (uint32_t t = lane; t < l1 - ri.loc; t += 32) cp_async4(&stage[ri.loc + t], res + ri.goff + t);
+    // every element of the tile is in flight at once.  Warp w owns runs w,
+    // w + WARPS, ...; their descriptors are loaded by one lane each, all at
+    // once, and handed round by shuffles (no load latency per run).
+    constexpr uint32_t WARPS = TT / 32;
+    for (uint32_t r0 = warp; r0 < rg.nreg; r0 += 32 * WARPS) {
+        const uint32_t reg = r0 + lane * WARPS;
+        uint32_t goff = 0, loc = 0, end = 0;
+        if (reg < rg.nreg) {
+            const RunInfo ri = tr[reg];
+            goff = ri.goff;
+            loc = ri.loc;
+            end = reg + 1 < rg.nreg ? tr[reg + 1].loc : tcount;
+        }
+        const uint32_t nrun = min(32u, (rg.nreg - r0 + WARPS - 1) / WARPS);
+        for (uint32_t j = 0; j < nrun; ++j) {
+            const uint32_t g = __shfl_sync(0xffffffffu, goff, j);
+            const uint32_t l = __shfl_sync(0xffffffffu, loc, j);
+            const uint32_t len = __shfl_sync(0xffffffffu, end, j) - l;
+            for (uint32_t t = lane; t < len; t += 32) cp_async4(&stage[l + t], res + g + t);
+        }
     }
     cp_async_commit();
     cp_async_wait<0>();
