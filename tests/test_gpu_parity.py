@@ -14,6 +14,7 @@ import pytest
 import oracle
 import paper_1903_00227_b200 as wrs
 from tests.stats_util import chi_square
+from tests.extreme import extreme_cases
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -150,6 +151,8 @@ def weight_cases(P):
         x[rng.random(n) < 0.5] = 1.0
         yield f"mixties_{n}", x
         yield f"skew_{n}", 10.0 ** rng.uniform(-12, 12, n)
+    for i, w in enumerate(extreme_cases()):
+        yield f"extreme{i}", w
 
 
 def test_random_tables_bit_exact(P):
@@ -190,6 +193,17 @@ def test_draws_bit_exact_random(P):
         S.draw_device(77, k, Wk, out)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+
+
+def test_draws_bit_exact_extreme_magnitudes(P):
+    # totals >= 1e300 (guarded compensated add), infinite total (coin = u * inf),
+    # subnormal weights; same cases the reference pins in test_ref_pins.py
+    for w in extreme_cases():
+        W, S = build(w, 3)
+        assert_same_table(S, w, 3, P)
+        for Wk in (1, 5):
+            ref = P.sample_many(S.buckets(), S.bucket_mean, 9, 40001, Wk)
+            assert np.array_equal(S.draw(9, 40001, Wk), ref), (w.size, Wk)
 
 
 def test_draw_zero_and_workers_zero(P):

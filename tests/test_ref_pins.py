@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
+from tests.extreme import extreme_cases
 
 R = oracle.ref()
 pytestmark = pytest.mark.skipif(R is None, reason="oracle/_ref not built")
@@ -24,6 +25,7 @@ def cases():
         x = rng.random(n)
         x[rng.random(n) < 0.3] = 1.0  # exact ties
         out.append(x + 1e-3)
+    out.extend(extreme_cases())
     return out
 
 
@@ -33,7 +35,7 @@ def test_port_equals_reference_build(jobs):
     for w in cases():
         a, wa = P.psa_build(w, jobs)
         b, wb = R.psa_build_jobs(w, jobs, 4)
-        assert wa == wb
+        assert wa == wb or (np.isnan(wa) and np.isnan(wb))
         assert a.tobytes() == b.tobytes(), (w.size, jobs)
         if jobs <= 8:  # the reference's own threaded ctor, one thread per job
             c, _ = R.psa_build(w, jobs)
@@ -65,6 +67,15 @@ def test_port_equals_reference_draws():
         b, wn = t.buckets()
         for W in (1, 3, 8, 13):
             assert np.array_equal(t.sample_many(7, 20011, W), P.sample_many(b, wn, 7, 20011, W))
+
+
+def test_port_equals_reference_draws_extreme():
+    P = oracle.port()
+    for w in extreme_cases():
+        t = R.table(w, 3)
+        b, wn = t.buckets()
+        for W in (1, 5):
+            assert np.array_equal(t.sample_many(9, 4001, W), P.sample_many(b, wn, 9, 4001, W))
 
 
 def test_port_equals_reference_generators_and_masses():
