@@ -324,29 +324,45 @@ __device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t 
 // is recorded (q order) for RD, so the (non-deterministic) order inside a run
 // never needs to be reproduced.
 __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t tile) {
-    const size_t head = (2 * static_cast<size_t>(nreg) + 1) * 4;
-    return ((head + 15) & ~size_t(15)) + tile * sizeof(uint2) + tile * sizeof(uint16_t);
+    const size_t head = (4 * static_cast<size_t>(nreg) + 2) * 4;
+    return ((head + 15) & ~size_t(15)) + tile * sizeof(uint2);
 }
 
 // ORDER = false (aggregated draws): the answers are only counted, never put
 // back in draw order, so the tile slots and the run table are not written.
-template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS>
-__global__ void __launch_bounds__(TT)
-k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restrict__ overflow,
-                 uint2* __restrict__ rec, uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
+// FULL: every tile of the launch holds TT * RS_ROWS draws, so no per-draw
+// bounds test is compiled (the one partial tile of a chunk, if any, is a
+// separate one-CTA launch with tile0 = its index).
+// Phases: (1) buckets + per-region counts (shared atomics, no return value,
+// so only the 16 buckets stay in registers); (2) warp 0 scans the counts while
+// the other warps claim slab space for the tile's runs (global atomics), so the
+// two latencies overlap; (3) each draw takes its staging slot with a second
+// shared atomic on its region's fill cursor; (4) the staged records go out
+// run by run as contiguous blocks.
+#ifndef RS_MIN_CTAS
+#define RS_MIN_CTAS 5  // 256-thread CTAs per SM the register budget must allow (48 regs)
+#endif
+template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS, bool FULL = false>
+__global__ void __launch_bounds__(TT, RS_MIN_CTAS * 256 / TT)
+k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
+                 unsigned* __restrict__ overflow, uint2* __restrict__ rec,
+                 uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
     extern __shared__ __align__(16) unsigned char rs_smem[];
-    uint32_t* loc = reinterpret_cast<uint32_t*>(rs_smem);  // counts, then run starts
-    uint32_t* goff = loc + rg.nreg + 1;
-    uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((2 * rg.nreg + 1) * 4 + 15) & ~15u));
-    uint16_t* regmap = reinterpret_cast<uint16_t*>(stage + (TT * RS_ROWS));  // region of each staged slot
-    const uint64_t tile = blockIdx.x;
+    const uint32_t nreg = rg.nreg;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(rs_smem);  // [nreg] draws per region
+    uint32_t* start = cnt + nreg;                          // [nreg + 1] run starts in the stage
+    uint32_t* fill = start + nreg + 1;                     // [nreg] fill cursors
+    uint32_t* goff = fill + nreg;                          // [nreg] slab base, then slab - stage offset
+    uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((4 * nreg + 2) * 4 + 15) & ~15u));
+    const uint64_t tile = static_cast<uint64_t>(tile0) + blockIdx.x;
     const uint64_t tbase = tile * (TT * RS_ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i <= rg.nreg; i += TT) loc[i] = 0;
+    for (uint32_t i = threadIdx.x; i < nreg; i += TT) cnt[i] = 0;
     __syncthreads();
 
-    uint32_t bk[RS_ROWS], rank[RS_ROWS];
-    const uint32_t kc_left = static_cast<uint32_t>(umin64(rg.kc - tbase, (TT * RS_ROWS)));
+    uint32_t bk[RS_ROWS];
+    const uint32_t kc_left =
+        FULL ? (TT * RS_ROWS) : static_cast<uint32_t>(umin64(rg.kc - tbase, (TT * RS_ROWS)));
     const uint32_t n32 = static_cast<uint32_t>(rg.g.n);
     if (W1) {
         // single worker: counter of draw q is key + (2q + 1) G, and the rows of
@@ -379,25 +395,43 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
         const uint32_t e = r * TT + threadIdx.x;
-        rank[r] = 0;
-        if (e < kc_left) rank[r] = atomicAdd(&loc[bk[r] >> rg.shift], 1u);
+        if (e < kc_left) atomicAdd(&cnt[bk[r] >> rg.shift], 1u);
     }
     __syncthreads();
     if (warp == 0) {  // exclusive scan of the region counts, 32 at a time
         uint32_t carry = 0;
-        for (uint32_t r0 = 0; r0 < rg.nreg; r0 += 32) {
+        for (uint32_t r0 = 0; r0 < nreg; r0 += 32) {
             const uint32_t reg = r0 + lane;
-            const uint32_t c = reg < rg.nreg ? loc[reg] : 0;
+            const uint32_t c = reg < nreg ? cnt[reg] : 0;
             uint32_t x = c;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            if (reg < rg.nreg) loc[reg] = carry + x - c;
+            if (reg < nreg) {
+                start[reg] = carry + x - c;
+                fill[reg] = carry + x - c;
+            }
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) loc[rg.nreg] = carry;
+        if (lane == 0) start[nreg] = carry;
+    } else {  // claim slab space for each non-empty run of this tile
+        for (uint32_t reg = threadIdx.x - 32; reg < nreg; reg += TT - 32) {
+            const uint32_t c = cnt[reg];
+            uint32_t g = 0;
+            if (c) {
+                const uint32_t base = atomicAdd(&cursor[reg], c);
+                if (base + c <= rg.cap) {
+                    g = reg * rg.cap + base;
+                } else {
+                    const uint32_t ob = atomicAdd(&cursor[nreg], c);
+                    if (ob + c > rg.ov_cap) atomicOr(overflow, 1u);
+                    g = nreg * rg.cap + (ob + c <= rg.ov_cap ? ob : 0);
+                }
+            }
+            goff[reg] = g;
+        }
     }
     __syncthreads();
     const uint32_t t32 = static_cast<uint32_t>(tbase);
@@ -405,44 +439,30 @@ k_region_scatter(RegionGeom rg, uint32_t* __restrict__ cursor, unsigned* __restr
     for (int r = 0; r < RS_ROWS; ++r) {
         const uint32_t e = r * TT + threadIdx.x;
         if (e < kc_left) {
-            const uint32_t reg = bk[r] >> rg.shift;
-            const uint32_t slot = loc[reg] + rank[r];
+            const uint32_t slot = atomicAdd(&fill[bk[r] >> rg.shift], 1u);
             stage[slot] = make_uint2(t32 + e, bk[r]);
-            regmap[slot] = static_cast<uint16_t>(reg);
             if (ORDER) slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
     }
-    // claim slab space for each non-empty run of this tile
-    for (uint32_t reg = threadIdx.x; reg < rg.nreg; reg += TT) {
-        const uint32_t c = loc[reg + 1] - loc[reg];
-        uint32_t g = 0;
-        if (c) {
-            const uint32_t base = atomicAdd(&cursor[reg], c);
-            if (base + c <= rg.cap) {
-                g = reg * rg.cap + base;
-            } else {
-                const uint32_t ob = atomicAdd(&cursor[rg.nreg], c);
-                if (ob + c > rg.ov_cap) atomicOr(overflow, 1u);
-                g = rg.nreg * rg.cap + (ob + c <= rg.ov_cap ? ob : 0);
-            }
-        }
-        goff[reg] = g - loc[reg];  // slab position of staged slot i = goff[region] + i
-        if (ORDER) runs[tile * rg.nreg + reg] = RunInfo{g, loc[reg]};
+    for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
+        const uint32_t g = goff[reg];
+        goff[reg] = g - start[reg];  // slab position of staged slot i = goff[region] + i
+        if (ORDER) runs[tile * nreg + reg] = RunInfo{g, start[reg]};
     }
     __syncthreads();
     // (no early exit on overflow: an overflowed run is written to the start
     // of the overflow slab, which stays in bounds, and RD recomputes the whole
     // chunk directly whenever the flag is set)
-    // staged tile -> slabs: slot i goes to goff[regmap[i]] + i, so consecutive
-    // slots of a run land on consecutive slab positions (one flat, fully
-    // unrolled pass; no per-run loop)
+    // staged tile -> slabs: slot i goes to goff[region of its bucket] + i, so
+    // consecutive slots of a run land on consecutive slab positions (one flat,
+    // fully unrolled pass; no per-run loop)
     const uint64_t pol = policy_evict_first();
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
         const uint32_t i = r * TT + threadIdx.x;
         if (i < kc_left) {
             const uint2 v = stage[i];
-            uint2* dst = rec + (goff[regmap[i]] + i);
+            uint2* dst = rec + (goff[v.y >> rg.shift] + i);
             asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
                          :: "l"(dst), "r"(v.x), "r"(v.y), "l"(pol));
         }
@@ -988,6 +1008,28 @@ void SampleWorkspace::release() {
     bytes = 0;
 }
 
+// RB over a chunk: the full tiles in one launch, the partial last tile (if
+// any) in a one-CTA launch of the bounds-checked variant.
+template <bool W1, bool ORDER, bool PHX, int TT>
+static void launch_scatter(const RegionGeom& rg, const RegionBuffers& B, int smem, cudaStream_t s) {
+    const uint64_t full = rg.kc / (static_cast<uint64_t>(TT) * RS_ROWS);
+    if (full) {
+        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, true>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        k_region_scatter<W1, ORDER, PHX, TT, true><<<static_cast<unsigned>(full), TT, smem, s>>>(
+            rg, 0u, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+    }
+    if (rg.ntiles > full) {
+        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_region_scatter<W1, ORDER, PHX, TT, false><<<1, TT, smem, s>>>(
+            rg, static_cast<uint32_t>(full), B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
+    }
+}
+
 // One chunk of the region plan with TT-thread tiles: RB (on the side stream
 // when asked), then RC and RD on st.
 template <int TT>
@@ -1003,22 +1045,12 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
     if (e != cudaSuccess) return e;
     const unsigned tiles = static_cast<unsigned>(rg.ntiles);
     const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
-    if (g.philox) {
-        cudaFuncSetAttribute(k_region_scatter<true, true, true, TT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-        k_region_scatter<true, true, true, TT><<<tiles, TT, sm_scatter, ss>>>(
-            rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-    } else if (w1) {
-        cudaFuncSetAttribute(k_region_scatter<true, true, false, TT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-        k_region_scatter<true, true, false, TT><<<tiles, TT, sm_scatter, ss>>>(
-            rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-    } else {
-        cudaFuncSetAttribute(k_region_scatter<false, true, false, TT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-        k_region_scatter<false, true, false, TT><<<tiles, TT, sm_scatter, ss>>>(
-            rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-    }
+    if (g.philox)
+        launch_scatter<true, true, true, TT>(rg, B, sm_scatter, ss);
+    else if (w1)
+        launch_scatter<true, true, false, TT>(rg, B, sm_scatter, ss);
+    else
+        launch_scatter<false, true, false, TT>(rg, B, sm_scatter, ss);
     if (on_side) {
         if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
@@ -1102,26 +1134,10 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
 template <bool W1>
 static cudaError_t count_scatter(int tt, const RegionGeom& rg, const RegionBuffers& B,
                                  int sm_scatter, cudaStream_t st) {
-    const unsigned tiles = static_cast<unsigned>(rg.ntiles);
     switch (tt) {
-        case 256:
-            cudaFuncSetAttribute(k_region_scatter<W1, false, false, 256>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-            k_region_scatter<W1, false, false, 256><<<tiles, 256, sm_scatter, st>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-            break;
-        case 512:
-            cudaFuncSetAttribute(k_region_scatter<W1, false, false, 512>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-            k_region_scatter<W1, false, false, 512><<<tiles, 512, sm_scatter, st>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-            break;
-        default:
-            cudaFuncSetAttribute(k_region_scatter<W1, false, false, 1024>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm_scatter);
-            k_region_scatter<W1, false, false, 1024><<<tiles, 1024, sm_scatter, st>>>(
-                rg, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
-            break;
+        case 256: launch_scatter<W1, false, false, 256>(rg, B, sm_scatter, st); break;
+        case 512: launch_scatter<W1, false, false, 512>(rg, B, sm_scatter, st); break;
+        default: launch_scatter<W1, false, false, 1024>(rg, B, sm_scatter, st); break;
     }
     return cudaGetLastError();
 }
