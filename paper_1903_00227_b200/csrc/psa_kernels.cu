@@ -669,7 +669,9 @@ struct K4Smem {
     double lw[32][K4_LW];     // light weight in, light alias (low word) out
     double hw[32][K4_HW];     // heavy weight in, heavy share out
     uint32_t hix[32][K4_HW];  // heavy id in, heavy alias out
+    uint4 desc[32];           // per-lane window / flush descriptor, read back as broadcasts
 };
+static_assert(K4_WARPS * sizeof(K4Smem) <= 232448, "K4a windows exceed 227 KB of shared memory");
 
 __device__ __forceinline__ uint32_t& low_word(double& d) { return reinterpret_cast<uint32_t*>(&d)[0]; }
 
@@ -705,26 +707,27 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
 
     while (__any_sync(0xffffffffu, state != ST_DONE)) {
         // ---- stage this phase's windows ------------------------------------
+        // Every lane posts its window (light start, heavy start, counts) to
+        // shared memory; the warp then copies row r with one broadcast read of
+        // lane r's descriptor (item indices fit 32 bits: n < 2^32).  hcnt <=
+        // K4_S + 2 = 32, so one copy per lane covers a heavy row.
         const bool live = state != ST_DONE;
         const uint64_t wl0 = i;
         const int lcnt = live ? static_cast<int>(umin64(K4_S, lhi - i)) : 0;
         const uint64_t wh0 = umin64(j, nh - 1);
         const uint64_t hend = umin64(umin64(j + K4_S + 1, hhi + 1), nh);
         const int hcnt = live ? static_cast<int>(hend - wh0) : 0;
-#pragma unroll 4
+        S.desc[lane] = make_uint4(static_cast<uint32_t>(wl0), static_cast<uint32_t>(wh0),
+                                  static_cast<uint32_t>(lcnt | (hcnt << 8)), 0u);
+        __syncwarp();
+#pragma unroll 8
         for (int r = 0; r < 32; ++r) {
-            const uint64_t rl0 = __shfl_sync(0xffffffffu, wl0, r);
-            const int rlc = __shfl_sync(0xffffffffu, lcnt, r);
-            const uint64_t rh0 = __shfl_sync(0xffffffffu, wh0, r);
-            const int rhc = __shfl_sync(0xffffffffu, hcnt, r);
-            if (lane < rlc) cp_async8(&S.lw[r][lane], lw + rl0 + lane);
+            const uint4 d = S.desc[r];
+            const int rlc = static_cast<int>(d.z & 0xffu), rhc = static_cast<int>(d.z >> 8);
+            if (lane < rlc) cp_async8(&S.lw[r][lane], lw + (d.x + lane));
             if (lane < rhc) {
-                cp_async8(&S.hw[r][lane], hw + rh0 + lane);
-                cp_async4(&S.hix[r][lane], hidx + rh0 + lane);
-            }
-            if (lane + 32 < rhc) {
-                cp_async8(&S.hw[r][lane + 32], hw + rh0 + lane + 32);
-                cp_async4(&S.hix[r][lane + 32], hidx + rh0 + lane + 32);
+                cp_async8(&S.hw[r][lane], hw + (d.y + lane));
+                cp_async4(&S.hix[r][lane], hidx + (d.y + lane));
             }
         }
         cp_async_commit();
@@ -831,17 +834,18 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
         const int nlw = static_cast<int>(i - i0);
         const int nhw = static_cast<int>(j - j0);
         const int hoff = static_cast<int>(j0 - wh0);
-#pragma unroll 2
+        S.desc[lane] = make_uint4(static_cast<uint32_t>(i0), static_cast<uint32_t>(j0),
+                                  static_cast<uint32_t>(nlw | (nhw << 8) | (hoff << 16)), 0u);
+        __syncwarp();
+#pragma unroll 8
         for (int r = 0; r < 32; ++r) {
-            const uint64_t rl0 = __shfl_sync(0xffffffffu, i0, r);
-            const uint64_t rj0 = __shfl_sync(0xffffffffu, j0, r);
-            const int rl = __shfl_sync(0xffffffffu, nlw, r);
-            const int rh = __shfl_sync(0xffffffffu, nhw, r);
-            const int ro = __shfl_sync(0xffffffffu, hoff, r);
-            if (lane < rl) lalias[rl0 + lane] = low_word(S.lw[r][lane]);
+            const uint4 d = S.desc[r];
+            const int rl = static_cast<int>(d.z & 0xffu), rh = static_cast<int>((d.z >> 8) & 0xffu);
+            const int ro = static_cast<int>(d.z >> 16);
+            if (lane < rl) lalias[d.x + lane] = low_word(S.lw[r][lane]);
             if (lane < rh) {
-                hshare[rj0 + lane] = S.hw[r][ro + lane];
-                halias[rj0 + lane] = S.hix[r][ro + lane];
+                hshare[d.y + lane] = S.hw[r][ro + lane];
+                halias[d.y + lane] = S.hix[r][ro + lane];
             }
         }
         __syncwarp();
