@@ -173,7 +173,11 @@ k_total(const double* __restrict__ w, uint64_t n, int D, double* node_val,
 // ballots of light / heavy flags and exclusive light / heavy offsets in index
 // order.
 // ===========================================================================
-constexpr int K1_THREADS = 256;
+#ifndef K1_THREADS_DEF
+#define K1_THREADS_DEF 256
+#endif
+constexpr int K1_THREADS = K1_THREADS_DEF;
+constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_ROWS = 16;
 constexpr int K1_TILE = K1_THREADS * K1_ROWS;  // 4096
 constexpr int K1_SLOTS = K1_ROWS * (K1_THREADS / 32);  // (row, warp) cells
@@ -211,8 +215,8 @@ __device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint
         const unsigned lm = __ballot_sync(0xffffffffu, light);
         const unsigned hm = __ballot_sync(0xffffffffu, valid && !light);
         if (lane == 0) {
-            C.lm[r * 8 + warp] = lm;
-            C.hm[r * 8 + warp] = hm;
+            C.lm[r * K1_WARPS + warp] = lm;
+            C.hm[r * K1_WARPS + warp] = hm;
         }
     }
     __syncthreads();
@@ -322,7 +326,7 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int r = 0; r < K1_ROWS; ++r) {
-        const int cell = r * 8 + warp;
+        const int cell = r * K1_WARPS + warp;
         const unsigned lm = C.lm[cell], hm = C.hm[cell];
         if ((lm >> lane) & 1) {
             sw[C.exL[cell] + __popc(lm & lt)] = xs[r];
@@ -897,7 +901,7 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     for (int r = 0; r < K1_ROWS; ++r) {
         const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
         if (gi >= n) continue;
-        const int cell = r * 8 + warp;
+        const int cell = r * K1_WARPS + warp;
         const unsigned lm = C.lm[cell];
         double share;
         uint32_t alias = static_cast<uint32_t>(gi);
