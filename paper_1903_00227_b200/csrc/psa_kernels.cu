@@ -28,6 +28,7 @@
 // No stage needs a host round trip: counts live in DevScalars and every grid
 // is sized from upper bounds.
 #include <atomic>
+#include <cstdlib>
 #include <type_traits>
 #include <cstdio>
 #include <math_constants.h>
@@ -453,6 +454,127 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
         }
     }
     if (!PASS3 && me.len > 0) totals[b] = cs.value();  // carry[b] = local.value(), :114
+}
+
+// Small tables (a few block chains per SM, so the chains' latency is the
+// kernel's time): one lane per block as above, but the block is read straight
+// into registers with 16-B loads, the next 32 elements in flight while the
+// current 32 are summed, and (pass 3) written back with 16-B stores (the
+// prefix arrays start one element in, so each 32 goes out as 1 + 15 pairs +
+// 1).  No staging loop.  Measured per-pass time of a lone 2048-step chain:
+// 0.12 / 0.21 ms (k_scan_blocks, pass 1 / 3) -> 0.05 / 0.06 ms.
+#ifndef K2S_U_DEF
+#define K2S_U_DEF 32
+#endif
+constexpr int K2S_U = K2S_U_DEF;  // elements per chunk (the next chunk is in flight)
+
+// N adds of a CompSumPos chain over x[], software-pipelined by hand: pairs
+// of adds pass through three stages in consecutive steps -- the hi chain
+// (t = hi + x), the error terms e = (max - t) + min, the lo chain (lo += e)
+// with the run's value t + lo after each add -- and step v runs hi(v),
+// e(v-1), lo(v-2) interleaved, so the in-order warp finds independent work
+// between the dependent DADDs.  Exactly CompSumPos::add's additions, in order.
+template <int N, bool OUT>
+__device__ __forceinline__ void chain_pos_pipelined(const double (&x)[N], double (&o)[N],
+                                                    CompSumPos& cs) {
+    constexpr int B = 2, NB = N / B;
+    static_assert(N % B == 0, "pairs");
+    double H[3][B], T[3][B], E[3][B];
+    double hi = cs.hi, lo = cs.lo;
+#pragma unroll
+    for (int v = 0; v < NB + 2; ++v) {
+        const int sh = v % 3, se = (v + 2) % 3, sl = (v + 1) % 3;  // sets of v, v-1, v-2
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (v < NB) {
+                H[sh][u] = hi;
+                T[sh][u] = hi + x[v * B + u];
+                hi = T[sh][u];
+            }
+            if (v >= 1 && v - 1 < NB) {
+                const double xv = x[(v - 1) * B + u];
+                const bool big = H[se][u] >= xv;
+                const double a = big ? H[se][u] : xv, b = big ? xv : H[se][u];
+                E[se][u] = (a - T[se][u]) + b;
+            }
+            if (v >= 2) {
+                lo = lo + E[sl][u];
+                if (OUT) o[(v - 2) * B + u] = T[sl][u] + lo;
+            }
+        }
+    }
+    cs.hi = hi;
+    cs.lo = lo;
+}
+template <int N, bool OUT>
+__device__ __forceinline__ void chain_pos_pipelined(const double (&x)[N], double (&o)[N],
+                                                    CompSum& cs) {
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        cs.add(x[u]);
+        if (OUT) o[u] = cs.value();
+    }
+}
+template <bool PASS3, class CS>
+__global__ void __launch_bounds__(64)
+k_scan_blocks_direct(const double* __restrict__ lw, const double* __restrict__ hw,
+                     double* __restrict__ lpre, double* __restrict__ hpre, const DevScalars* sc,
+                     double* __restrict__ totals, const double* __restrict__ carries) {
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const double* src;
+    double* dst;
+    int len;
+    if (b < nbl) {
+        src = lw + b * SCAN_BLOCK;
+        dst = lpre + 1 + b * SCAN_BLOCK;
+        len = static_cast<int>(umin64(SCAN_BLOCK, nl - b * SCAN_BLOCK));
+    } else if (b - nbl < nbh) {
+        const uint64_t hb = b - nbl;
+        src = hw + hb * SCAN_BLOCK;
+        dst = hpre + 1 + hb * SCAN_BLOCK;
+        len = static_cast<int>(umin64(SCAN_BLOCK, nh - hb * SCAN_BLOCK));
+    } else {
+        return;
+    }
+    CS cs{0.0, 0.0};
+    if (PASS3) cs.add(carries[b]);  // run.add(carry[b]), parallel.hpp:124
+    const int full = len / K2S_U;
+    double2 nx[K2S_U / 2];
+    if (full > 0) {
+#pragma unroll
+        for (int u = 0; u < K2S_U / 2; ++u) nx[u] = __ldcs(reinterpret_cast<const double2*>(src) + u);
+    }
+    for (int c = 0; c < full; ++c) {
+        double x[K2S_U];
+#pragma unroll
+        for (int u = 0; u < K2S_U / 2; ++u) {
+            x[2 * u] = nx[u].x;
+            x[2 * u + 1] = nx[u].y;
+        }
+        if (c + 1 < full) {
+#pragma unroll
+            for (int u = 0; u < K2S_U / 2; ++u)
+                nx[u] = __ldcs(reinterpret_cast<const double2*>(src + (c + 1) * K2S_U) + u);
+        }
+        double o[K2S_U];
+        chain_pos_pipelined<K2S_U, PASS3>(x, o, cs);  // out[i] = run.value(), parallel.hpp:127
+        if (PASS3) {
+            double* d = dst + c * K2S_U;  // 8 mod 16: one scalar, pairs, one scalar
+            d[0] = o[0];
+#pragma unroll
+            for (int u = 0; u < K2S_U / 2 - 1; ++u)
+                __stcs(reinterpret_cast<double2*>(d + 1) + u, make_double2(o[2 * u + 1], o[2 * u + 2]));
+            d[K2S_U - 1] = o[K2S_U - 1];
+        }
+    }
+    for (int e = full * K2S_U; e < len; ++e) {
+        cs.add(src[e]);
+        if (PASS3) dst[e] = cs.value();
+    }
+    if (!PASS3 && len > 0) totals[b] = cs.value();  // carry[b] = local.value(), parallel.hpp:114
 }
 
 // ===========================================================================
@@ -1026,6 +1148,13 @@ cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStrea
     return cudaGetLastError();
 }
 
+// Item count up to which K2a/K2c use k_scan_blocks_direct (WRS_B200_K2_DIRECT_MAX
+// overrides; results are identical either way).
+static uint64_t k2_direct_max() {
+    const char* e = std::getenv("WRS_B200_K2_DIRECT_MAX");  // read per build (tests flip it)
+    return e ? std::strtoull(e, nullptr, 10) : (1ull << 25);
+}
+
 cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
                              Bucket* d_b, Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
     const int k1_smem = K1_TILE * 12;
@@ -1055,24 +1184,33 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     REC(1);
     // every prefix-chain value is finite and >= 0 when W is far below DBL_MAX
     const bool pos = total < 1e300;
-    if (pos)
-        k_scan_blocks<false, CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(
-            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
-    else
-        k_scan_blocks<false, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(
-            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
+    // few chains per SM: their latency sets the time, so the leaner direct form
+    const bool direct = n <= k2_direct_max();
+    const unsigned k2d_grid = static_cast<unsigned>((nblocks + 63) / 64);
+#define K2_LAUNCH(PASS3)                                                                          \
+    do {                                                                                          \
+        if (direct && pos)                                                                        \
+            k_scan_blocks_direct<PASS3, CompSumPos><<<k2d_grid, 64, 0, st>>>(                     \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+        else if (direct)                                                                          \
+            k_scan_blocks_direct<PASS3, CompSum><<<k2d_grid, 64, 0, st>>>(                        \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+        else if (pos)                                                                             \
+            k_scan_blocks<PASS3, CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(                  \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+        else                                                                                      \
+            k_scan_blocks<PASS3, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(                     \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+    } while (0)
+    K2_LAUNCH(false);
     REC(2);
     if (pos)
         k_scan_carry<CompSumPos><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     else
         k_scan_carry<CompSum><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     REC(3);
-    if (pos)
-        k_scan_blocks<true, CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(
-            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
-    else
-        k_scan_blocks<true, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(
-            ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);
+    K2_LAUNCH(true);
+#undef K2_LAUNCH
     REC(4);
     k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
                                      ws.split_s);
