@@ -1,6 +1,6 @@
 """BASELINE configs[4] on one B200: size sweep n = 2^10 .. 2^30 (powers of 4)
 for Uniform(0,1] (generate_uniform, on the device) and power-law s=0.5
-(generate_powerlaw, host shuffle), build time (rebuild alone, median of
+(generate_powerlaw: host pow, Fisher-Yates deal on the device), build time (rebuild alone, median of
 reps) and 1e9-draw query throughput per size, each with its HBM roofline
 fraction (72 B/item build, 36 B/sample draws) and whether the 16n-B table is
 L2-resident.
@@ -23,8 +23,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--draws", type=int, default=10**9)
     ap.add_argument("--max-log2", type=int, default=30)
-    ap.add_argument("--powerlaw-max-log2", type=int, default=28,
-                    help="the power-law generator shuffles on the host; cap its size")
+    ap.add_argument("--powerlaw-max-log2", type=int, default=30,
+                    help="cap the power-law sizes (its (i+1)^-s values are computed on the host)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default="profiles/r01_size_sweep")
     args = ap.parse_args()
