@@ -17,7 +17,8 @@
 //           HBM-resident table moves a full 128-B line (ncu: 126 B/draw), so
 //           the direct plan tops out near 6.5 TB/s / 132 B = 50 G draws/s.
 //           The region plan reorders the WORK, not the results: draws are
-//           bucketed by table region (2^21 buckets = 32 MB, L2-resident) with
+//           bucketed by table region (2^21 buckets = 32 MB, L2-resident;
+//           64 MB above 2^27 buckets, region_shift) with
 //           a tile-local counting sort into per-region slabs (space claimed by
 //           atomics), the gathers then sweep the table region by region so
 //           every line is fetched from HBM about once, and a final pass puts
@@ -901,10 +902,23 @@ static int sm_count() {
     return sms;
 }
 
-static int region_shift() { return 21; }  // 2^21 buckets = 32 MB per region
+// Region = 2^shift buckets: 32 MB regions up to 2^27 buckets, 64 MB above.
+// Measured (1e9 draws, scripts/draw_probe.py): 32 MB wins at n <= 2^26 (8.86
+// vs 9.19 ms at 2^26: the 64-MB region crowds the L2 during the gather), the
+// two tie at 2^27, 64 MB wins above (9.72 vs 10.19 ms at 2e8, 13.30 vs 15.22
+// at 2^30: half the regions, so longer runs per tile and half the per-tile
+// scan / claim / run-table work).  WRS_B200_REGION_SHIFT overrides.
+static int region_shift(uint64_t n) {
+    if (const char* env = getenv("WRS_B200_REGION_SHIFT")) {
+        const int v = atoi(env);
+        if (v >= 16 && v <= 24) return v;
+    }
+    return n > (1ull << 27) ? 22 : 21;
+}
 
 bool use_region_plan(uint64_t n, uint64_t k) {
-    const uint64_t nreg = (n + (1ull << region_shift()) - 1) >> region_shift();
+    const int sh = region_shift(n);
+    const uint64_t nreg = (n + (1ull << sh) - 1) >> sh;
     if (const char* env = getenv("WRS_B200_PLAN")) {  // experiments: force a plan
         if (env[0] == 'd') return false;
         if (env[0] == 'r') return nreg <= RS_MAX_REGIONS;
@@ -936,7 +950,7 @@ static int tile_threads_for(uint32_t nreg) {
 static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     RegionPlan p{};
     p.rg.g = g;
-    p.rg.shift = region_shift();
+    p.rg.shift = region_shift(g.n);
     p.rg.nreg = static_cast<uint32_t>((g.n + (1ull << p.rg.shift) - 1) >> p.rg.shift);
     // expected draws per full region + ~20 sigma + a tile of slack
     const double mu = static_cast<double>(chunk) *

@@ -306,11 +306,13 @@ def test_full_size_table_and_draws(P):
 
 # ---- region-ordered draw plan (table beyond L2) ---------------------------------------
 
-@pytest.mark.parametrize("chunk", [None, 3_000_001])
-def test_region_plan_draws_bit_exact(P, chunk, monkeypatch):
+@pytest.mark.parametrize("chunk,shift", [(None, None), (3_000_001, None), (None, 22), (None, 19)])
+def test_region_plan_draws_bit_exact(P, chunk, shift, monkeypatch):
     import torch
     if chunk:
         monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
+    if shift:  # 64-MB regions (the default above 2^27 buckets) / many small regions
+        monkeypatch.setenv("WRS_B200_REGION_SHIFT", str(shift))
     n = 9_500_003  # 152 MB table: region plan
     w = P.generate_powerlaw(n, 0.5, 11)
     W, S = build(w)
