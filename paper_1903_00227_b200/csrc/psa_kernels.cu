@@ -519,11 +519,15 @@ template <bool PASS3, class CS>
 __global__ void __launch_bounds__(64)
 k_scan_blocks_direct(const double* __restrict__ lw, const double* __restrict__ hw,
                      double* __restrict__ lpre, double* __restrict__ hpre, const DevScalars* sc,
-                     double* __restrict__ totals, const double* __restrict__ carries) {
+                     double* __restrict__ totals, const double* __restrict__ carries, int lpw) {
     const uint64_t nl = sc->nl, nh = sc->nh;
     const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
     const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
-    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // lpw chains per warp: fewer lanes per warp spread the chains over more
+    // schedulers (each SMSP's FP64 pipe serves 16 lanes per cycle)
+    const int lane = threadIdx.x & 31;
+    if (lane >= lpw) return;
+    const uint64_t b = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * lpw + lane;
     const double* src;
     double* dst;
     int len;
@@ -1148,6 +1152,19 @@ cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStrea
     return cudaGetLastError();
 }
 
+// Chains per warp of k_scan_blocks_direct (WRS_B200_K2_LPW: experiments).
+static int k2_direct_lpw(uint64_t nblocks) {
+    if (const char* e = std::getenv("WRS_B200_K2_LPW")) {
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= 32) return v;
+    }
+    // measured (scripts/stage_probe.py): one chain per warp up to ~1e3
+    // chains, then about 1024-1280 warps (lpw 2 at 2^22 items, 8 at 2^24)
+    int lpw = 1;
+    while (lpw < 32 && static_cast<uint64_t>(lpw) * 1280 < nblocks) lpw <<= 1;
+    return lpw;
+}
+
 // Item count up to which K2a/K2c use k_scan_blocks_direct (WRS_B200_K2_DIRECT_MAX
 // overrides; results are identical either way).
 static uint64_t k2_direct_max() {
@@ -1186,15 +1203,16 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     const bool pos = total < 1e300;
     // few chains per SM: their latency sets the time, so the leaner direct form
     const bool direct = n <= k2_direct_max();
-    const unsigned k2d_grid = static_cast<unsigned>((nblocks + 63) / 64);
+    const int lpw = k2_direct_lpw(nblocks);
+    const unsigned k2d_grid = static_cast<unsigned>((nblocks + 2 * lpw - 1) / (2 * lpw));
 #define K2_LAUNCH(PASS3)                                                                          \
     do {                                                                                          \
         if (direct && pos)                                                                        \
             k_scan_blocks_direct<PASS3, CompSumPos><<<k2d_grid, 64, 0, st>>>(                     \
-                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries, lpw);               \
         else if (direct)                                                                          \
             k_scan_blocks_direct<PASS3, CompSum><<<k2d_grid, 64, 0, st>>>(                        \
-                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries, lpw);               \
         else if (pos)                                                                             \
             k_scan_blocks<PASS3, CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(                  \
                 ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
