@@ -83,13 +83,15 @@ def test_sample_with_replacement_like_reference_capi():  # test_capi.cpp:80-112
                                          C.byref(m)) == 1  # WRS_EINVAL
 
 
-@pytest.mark.parametrize("chunk", [None, 3_000_001])
-def test_counts_region_plan_match_device_draws(P, chunk, monkeypatch):
+@pytest.mark.parametrize("chunk,shift", [(None, None), (3_000_001, None), (None, 22)])
+def test_counts_region_plan_match_device_draws(P, chunk, shift, monkeypatch):
     """HBM-resident table (region plan); the device draws themselves are pinned
     bit-exact to the oracle in test_gpu_parity."""
     import torch
     if chunk:
         monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
+    if shift:  # 64-MB regions, the default above 2^27 buckets
+        monkeypatch.setenv("WRS_B200_REGION_SHIFT", str(shift))
     n = 9_500_003
     w = P.generate_powerlaw(n, 0.5, 11)
     W = wrs.Weights.from_array(w)
