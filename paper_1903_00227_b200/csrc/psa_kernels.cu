@@ -656,6 +656,147 @@ __device__ __forceinline__ int carry_chain_pos(const double* in, double* out, in
     return v * B;
 }
 
+// K2b for CompSumPos, split over warps: one CTA per list, whose warps run the
+// parts of the compensated chain concurrently on different schedulers, chunk
+// by chunk (a CTA barrier between steps):
+//   warp 0  streams chunk c+1 of the totals into shared memory;
+//   warp 1  the hi chain of chunk c:        T[k] = hi = hi + x[k];
+//   warp 2  the error terms of chunk c-1:   e[k] = (max(H, x) - T) + min(H, x),
+//           H[k] = T[k-1] (the hi before the add), all lanes;
+//   warp 3  the lo chain of chunk c-2:      L[k] = lo, lo = lo + e[k];
+//   warp 4  the carries of chunk c-3:       carry[k] = H[k] + L[k], all lanes,
+//           coalesced stores.
+// The two sequential chains are one dependent DADD per total each, so a step
+// costs about one FP64 latency per total instead of a whole compensated add
+// issued by one warp (chain_bench: 8.3 vs 22 cycles).  The same additions as
+// CompSumPos::add, in the same order: carries are bit-identical.
+constexpr int K2W_S = 1024;               // totals per chunk
+constexpr int K2W_SMEM = 11 * K2W_S * 8 + 4 * 8;  // x ring 3, T ring 4, e ring 2, L ring 2, hin ring 4
+__global__ void __launch_bounds__(160)
+k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, double* carries,
+                   double* lpre, double* hpre) {
+    extern __shared__ __align__(16) double k2w[];
+    double* X = k2w;             // [3][S] totals
+    double* T = X + 3 * K2W_S;   // [4][S] hi after each add
+    double* E = T + 4 * K2W_S;   // [2][S] error terms
+    double* L = E + 2 * K2W_S;   // [2][S] lo before each add
+    double* hin = L + 2 * K2W_S;  // [4] hi entering each chunk
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const bool heavy = blockIdx.x == 1;
+    const uint64_t nb = heavy ? nbh : nbl;
+    const uint64_t off = heavy ? nbl : 0;
+    if (threadIdx.x == 0) (heavy ? hpre : lpre)[0] = 0.0;  // prefix[0] = 0, alias.hpp:89
+    if (nb == 0) return;
+    const double* src = totals + off;
+    double* dst = carries + off;
+    const int nch = static_cast<int>((nb + K2W_S - 1) / K2W_S);
+    auto cnt_of = [&](int c) {
+        return static_cast<int>(umin64(K2W_S, nb - static_cast<uint64_t>(c) * K2W_S));
+    };
+    auto load = [&](int c) {
+        if (c < nch) {
+            const int cnt = cnt_of(c);
+            double* xb = X + (c % 3) * K2W_S;
+            for (int i = lane; i < cnt; i += 32)
+                cp_async8(xb + i, src + static_cast<uint64_t>(c) * K2W_S + i);
+        }
+        cp_async_commit();
+    };
+    // H[k] of chunk c: the hi entering total k
+    auto h_at = [&](int c, int k) {
+        return k ? T[(c % 4) * K2W_S + k - 1] : hin[c % 4];
+    };
+    double hi = 0.0, lo = 0.0;  // warp 1 / warp 3, lane 0
+    if (warp == 0) {
+        load(0);
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    for (int it = 0; it < nch + 3; ++it) {
+        if (warp == 0) {
+            load(it + 1);  // read by warp 1 next step
+        } else if (warp == 1) {
+            const int c = it;
+            if (c < nch && lane == 0) {
+                const int cnt = cnt_of(c);
+                const double* __restrict__ xb = X + (c % 3) * K2W_S;
+                double* __restrict__ tb = T + (c % 4) * K2W_S;
+                hin[c % 4] = hi;
+                int k = 0;
+                for (; k + 16 <= cnt; k += 16) {  // loads first: the rings never alias
+                    double x[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) x[u] = xb[k + u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        hi = hi + x[u];
+                        x[u] = hi;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) tb[k + u] = x[u];
+                }
+                for (; k < cnt; ++k) {
+                    hi = hi + xb[k];
+                    tb[k] = hi;
+                }
+            }
+        } else if (warp == 2) {
+            const int c = it - 1;
+            if (c >= 0 && c < nch) {
+                const int cnt = cnt_of(c);
+                const double* xb = X + (c % 3) * K2W_S;
+                const double* tb = T + (c % 4) * K2W_S;
+                double* eb = E + (c % 2) * K2W_S;
+                for (int k = lane; k < cnt; k += 32) {
+                    const double h = h_at(c, k), x = xb[k];
+                    const bool big = h >= x;  // CompSumPos::add
+                    const double a = big ? h : x, b = big ? x : h;
+                    eb[k] = (a - tb[k]) + b;
+                }
+            }
+        } else if (warp == 3) {
+            const int c = it - 2;
+            if (c >= 0 && c < nch && lane == 0) {
+                const int cnt = cnt_of(c);
+                const double* __restrict__ eb = E + (c % 2) * K2W_S;
+                double* __restrict__ lb = L + (c % 2) * K2W_S;
+                int k = 0;
+                for (; k + 16 <= cnt; k += 16) {
+                    double e[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) e[u] = eb[k + u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const double l = lo;
+                        lo = lo + e[u];
+                        e[u] = l;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) lb[k + u] = e[u];
+                }
+                for (; k < cnt; ++k) {
+                    lb[k] = lo;
+                    lo = lo + eb[k];
+                }
+            }
+        } else {
+            const int c = it - 3;
+            if (c >= 0 && c < nch) {
+                const int cnt = cnt_of(c);
+                const double* lb = L + (c % 2) * K2W_S;
+                double* out = dst + static_cast<uint64_t>(c) * K2W_S;
+                for (int k = lane; k < cnt; k += 32)
+                    out[k] = h_at(c, k) + lb[k];  // carry[b] = acc.value(), parallel.hpp:116-121
+            }
+        }
+        if (warp == 0) cp_async_wait<0>();
+        __syncthreads();
+    }
+}
+
 template <class CS>
 __global__ void __launch_bounds__(32)
 k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* carries,
@@ -1179,6 +1320,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     // per-device attribute; cheap enough to set on every build
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
     cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
+    cudaFuncSetAttribute(k_scan_carry_split, cudaFuncAttributeMaxDynamicSharedMemorySize, K2W_SMEM);
     cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, K1_TILE * 12 + 16);
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
@@ -1223,7 +1365,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     K2_LAUNCH(false);
     REC(2);
     if (pos)
-        k_scan_carry<CompSumPos><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
+        k_scan_carry_split<<<2, 160, K2W_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     else
         k_scan_carry<CompSum><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     REC(3);
