@@ -190,7 +190,7 @@ def test_default_psa_is_reference_at_default_jobs(P):
 def test_draws_bit_exact_random(P):
     import torch
     for n, k, Wk in ((1, 1000, 1), (17, 12345, 3), (1000, 10**6, 8), (100_000, 3 * 10**6 + 7, 13),
-                     (4097, 5, 16)):
+                     (4097, 5, 16), (1000, 7, 1000), (1000, 100_003, 65_536), (2, 10, 3)):
         w = P.generate_powerlaw(n, 1.0, 3) if n > 1 else np.array([2.0])
         W, S = build(w)
         b = S.buckets()
