@@ -263,13 +263,16 @@ __device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint
 //   The light ids are never materialised: K4b recovers them from the tile
 //   prefix counts this kernel leaves in `status`.
 // ===========================================================================
-__global__ void __launch_bounds__(K1_THREADS)
+#ifndef K1_MIN_CTAS
+#define K1_MIN_CTAS 5  // 48 registers, 42 KB of shared memory: 5 CTAs per SM
+#endif
+__global__ void __launch_bounds__(K1_THREADS, K1_MIN_CTAS)
 k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
             unsigned long long* status, double* __restrict__ lw, uint32_t* __restrict__ hidx,
             double* __restrict__ hw) {
     extern __shared__ __align__(16) unsigned char k1_smem[];
     double* sw = reinterpret_cast<double*>(k1_smem);              // K1_TILE
-    uint32_t* sidx = reinterpret_cast<uint32_t*>(sw + K1_TILE);   // K1_TILE
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(sw + K1_TILE);   // K1_TILE tile-local ids
     __shared__ TileCells C;
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_excl;
@@ -333,7 +336,7 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
             sw[C.exL[cell] + __popc(lm & lt)] = xs[r];
         } else if ((hm >> lane) & 1) {
             const uint32_t p = totL + C.exH[cell] + __popc(hm & lt);
-            sidx[p] = static_cast<uint32_t>(base + r * K1_THREADS + threadIdx.x);
+            sidx[p] = static_cast<uint16_t>(r * K1_THREADS + threadIdx.x);
             sw[p] = xs[r];
         }
     }
@@ -341,7 +344,7 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
     const uint64_t L0 = s_excl, H0 = base - s_excl;
     for (uint32_t p = tid; p < totL; p += K1_THREADS) lw[L0 + p] = sw[p];
     for (uint32_t p = tid; p < totH; p += K1_THREADS) {
-        hidx[H0 + p] = sidx[totL + p];
+        hidx[H0 + p] = static_cast<uint32_t>(base + sidx[totL + p]);
         hw[H0 + p] = sw[totL + p];
     }
 }
@@ -1139,7 +1142,8 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     // The tile's lights are the contiguous light-list run [L0, L0 + totL) and
     // its heavies the run [H0, H0 + totH): both runs are staged into shared
     // memory with coalesced async copies, then every item reads its alias /
-    // share from there (no dependent global gathers).
+    // share from there (measured: reading them straight from global memory,
+    // at 7 CTAs/SM instead of 4, is slower: 0.70 vs 0.65 ms at n = 1e8).
     extern __shared__ __align__(16) unsigned char k4b_smem[];
     __shared__ TileCells C;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1315,7 +1319,7 @@ static uint64_t k2_direct_max() {
 
 cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
                              Bucket* d_b, Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
-    const int k1_smem = K1_TILE * 12;
+    const int k1_smem = K1_TILE * 10;
     const int k4_smem = K4_WARPS * static_cast<int>(sizeof(K4Smem));
     // per-device attribute; cheap enough to set on every build
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
