@@ -1134,6 +1134,10 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
 //   Ranks come from the same tile classification as K1 plus K1's inclusive
 //   tile prefix; every warp stores 32 consecutive buckets = 512 contiguous B.
 // ===========================================================================
+#ifndef K4B_SMEM_KB
+#define K4B_SMEM_KB 40
+#endif
+constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // staging budget: 5 CTAs per SM at 40 KB
 __global__ void __launch_bounds__(K1_THREADS)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
            const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lalias,
@@ -1154,14 +1158,23 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     const uint32_t totL = C.totL, totH = C.totH;
     const uint64_t L0 = (status[tile] & VAL_MASK) - totL;
     const uint64_t H0 = base - L0;
-    uint32_t* s_la = reinterpret_cast<uint32_t*>(k4b_smem);
-    double* s_hs = reinterpret_cast<double*>(k4b_smem + ((4u * totL + 15u) & ~15u));
-    uint32_t* s_ha = reinterpret_cast<uint32_t*>(s_hs + totH);
-    if (!uniform) {
-        for (uint32_t i = threadIdx.x; i < totL; i += K1_THREADS) cp_async4(&s_la[i], lalias + L0 + i);
+    // staged when the tile's runs fit the budget (every tile but nearly-all-
+    // heavy ones), else read straight from global memory
+    const bool staged = ((4u * totL + 15u) & ~15u) + 12u * totH <= K4B_SMEM;
+    const uint32_t* s_la = lalias + L0;
+    const double* s_hs = hshare + H0;
+    const uint32_t* s_ha = halias + H0;
+    if (!uniform && staged) {
+        uint32_t* d_la = reinterpret_cast<uint32_t*>(k4b_smem);
+        double* d_hs = reinterpret_cast<double*>(k4b_smem + ((4u * totL + 15u) & ~15u));
+        uint32_t* d_ha = reinterpret_cast<uint32_t*>(d_hs + totH);
+        s_la = d_la;
+        s_hs = d_hs;
+        s_ha = d_ha;
+        for (uint32_t i = threadIdx.x; i < totL; i += K1_THREADS) cp_async4(&d_la[i], lalias + L0 + i);
         for (uint32_t i = threadIdx.x; i < totH; i += K1_THREADS) {
-            cp_async8(&s_hs[i], hshare + H0 + i);
-            cp_async4(&s_ha[i], halias + H0 + i);
+            cp_async8(&d_hs[i], hshare + H0 + i);
+            cp_async4(&d_ha[i], halias + H0 + i);
         }
         cp_async_commit();
         cp_async_wait<0>();
@@ -1325,7 +1338,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
     cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
     cudaFuncSetAttribute(k_scan_carry_split, cudaFuncAttributeMaxDynamicSharedMemorySize, K2W_SMEM);
-    cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, K1_TILE * 12 + 16);
+    cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, K4B_SMEM);
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
     const unsigned k2_grid = static_cast<unsigned>((nblocks + K2_WARPS * 32 - 1) / (K2_WARPS * 32));
@@ -1383,7 +1396,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
                                                     ws.split_h, ws.split_s, ws.lalias, ws.hshare,
                                                     ws.halias);
     REC(6);
-    k_assemble<<<static_cast<unsigned>(ntiles), K1_THREADS, K1_TILE * 12 + 16, st>>>(
+    k_assemble<<<static_cast<unsigned>(ntiles), K1_THREADS, K4B_SMEM, st>>>(
         d_w, n, ws.sc, ws.tile_status, ws.lalias, ws.hshare, ws.halias, d_b);
     REC(7);
 #undef REC

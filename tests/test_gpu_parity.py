@@ -158,6 +158,8 @@ def weight_cases(P):
         x[rng.random(n) < 0.5] = 1.0
         yield f"mixties_{n}", x
         yield f"skew_{n}", 10.0 ** rng.uniform(-12, 12, n)
+        # sorted: whole 4096-item tiles of heavies (K4b's unstaged path) then of lights
+        yield f"sorted_{n}", np.sort(rng.random(n) + 0.01)[::-1].copy()
     for i, w in enumerate(extreme_cases()):
         yield f"extreme{i}", w
 
