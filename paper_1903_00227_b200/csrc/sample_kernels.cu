@@ -340,6 +340,12 @@ __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t til
 // two latencies overlap; (3) each draw takes its staging slot with a second
 // shared atomic on its region's fill cursor; (4) the staged records go out
 // run by run as contiguous blocks.
+#ifndef RC_MIN_CTAS
+#define RC_MIN_CTAS 7  // gather / count CTAs per SM the register budget must allow (32 regs)
+#endif
+#ifndef RD_MIN_CTAS
+#define RD_MIN_CTAS 8  // unpermute (256-thread) CTAs per SM (32 regs)
+#endif
 #ifndef RS_MIN_CTAS
 #define RS_MIN_CTAS 5  // 256-thread CTAs per SM the register budget must allow (48 regs)
 #endif
@@ -475,7 +481,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
 // GPU sweep the table region by region; table loads are marked evict-last,
 // record / result streams evict-first.
 template <bool W1, bool PHX = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RC_MIN_CTAS)
 k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
                 const uint2* __restrict__ rec, uint32_t* __restrict__ res) {
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 2048;
@@ -533,7 +539,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 // overflowed (not expected: ~20 sigma of slack), the tile recomputes its
 // draws directly instead, so the output is correct in every case.
 template <bool W1, bool PHX = false, int TT = RS_THREADS>
-__global__ void __launch_bounds__(TT)
+__global__ void __launch_bounds__(TT, RD_MIN_CTAS * 256 / TT)
 k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
                    const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
                    const uint16_t* __restrict__ slot_of, const uint32_t* __restrict__ res,
@@ -630,7 +636,7 @@ __device__ __forceinline__ void count_hit(uint32_t* hits, uint64_t n, uint32_t b
 }
 
 template <bool W1, bool PHX = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RC_MIN_CTAS)
 k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
                const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
                uint32_t* __restrict__ hits) {
