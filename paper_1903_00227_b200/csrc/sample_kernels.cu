@@ -340,6 +340,10 @@ __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t til
 // two latencies overlap; (3) each draw takes its staging slot with a second
 // shared atomic on its region's fill cursor; (4) the staged records go out
 // run by run as contiguous blocks.
+#ifndef RC_ROWS
+#define RC_ROWS 8  // records per gather / count thread
+#endif
+constexpr int RC_SPAN = RC_ROWS * 256;  // slab positions per gather / count CTA
 #ifndef RC_MIN_CTAS
 #define RC_MIN_CTAS 7  // gather / count CTAs per SM the register budget must allow (32 regs)
 #endif
@@ -477,14 +481,14 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
 }
 
 // RC: slab by slab, the coin flip of every record against its bucket.  One
-// contiguous run of 2048 slab positions per CTA, so the resident CTAs of the
+// contiguous run of RC_SPAN slab positions per CTA, so the resident CTAs of the
 // GPU sweep the table region by region; table loads are marked evict-last,
 // record / result streams evict-first.
 template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(256, RC_MIN_CTAS)
 k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
                 const uint2* __restrict__ rec, uint32_t* __restrict__ res) {
-    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 2048;
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
     const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);  // nreg = overflow slab
     const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
     const uint64_t valid_end =
@@ -493,18 +497,18 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
     const uint64_t key0 = rng_derive(rg.g.base_key, 0);  // W1: the single worker's key
-    uint2 r[8];
+    uint2 r[RC_ROWS];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
     }
     // bucket gathers as LDGSTS into shared memory: measured 232 G random
     // L2-resident 16-B rows/s vs 200 G for LDG (scripts/microbench/
     // l2_gather_bench.cu); each thread reads back only its own rows
-    __shared__ uint4 bk_s[8 * 256];
+    __shared__ uint4 bk_s[RC_ROWS * 256];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < RC_ROWS; ++u) {
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
         asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
                      ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
@@ -512,7 +516,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     cp_async_commit();
     cp_async_wait<0>();
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
         if (p < valid_end) {
@@ -641,7 +645,7 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
                const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
                uint32_t* __restrict__ hits) {
     if (*overflow) return;  // k_count_direct<.., true> recounts the chunk
-    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 2048;
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
     const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);
     const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
     const uint64_t valid_end =
@@ -650,15 +654,15 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
     const uint64_t key0 = rng_derive(rg.g.base_key, 0);
-    uint2 r[8];
+    uint2 r[RC_ROWS];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
     }
-    __shared__ uint4 bk_s[8 * 256];
+    __shared__ uint4 bk_s[RC_ROWS * 256];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < RC_ROWS; ++u) {
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
         asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
                      ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
@@ -666,7 +670,7 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
     cp_async_commit();
     cp_async_wait<0>();
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
         if (p < valid_end) {
@@ -964,8 +968,8 @@ static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     p.tt = tile_threads_for(p.rg.nreg);
     p.tile = static_cast<uint32_t>(p.tt * RS_ROWS);
     const double cap = mu + 20.0 * std::sqrt(mu) + 2.0 * p.tile;
-    // slabs are whole multiples of the gather CTA's 2048 positions
-    auto round2k = [](uint64_t x) { return static_cast<uint32_t>((x + 2047) & ~uint64_t(2047)); };
+    // slabs are whole multiples of the gather CTA's RC_SPAN positions
+    auto round2k = [](uint64_t x) { return static_cast<uint32_t>((x + RC_SPAN - 1) / RC_SPAN * RC_SPAN); };
     p.rg.cap = round2k(static_cast<uint64_t>(cap < static_cast<double>(chunk) ? cap : chunk) + p.tile);
     p.rg.ov_cap = round2k(chunk / 64 + 8 * p.tile);
     p.rec_slots = static_cast<uint64_t>(p.rg.nreg) * p.rg.cap + p.rg.ov_cap;
@@ -1064,7 +1068,7 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
     cudaError_t e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, ss);
     if (e != cudaSuccess) return e;
     const unsigned tiles = static_cast<unsigned>(rg.ntiles);
-    const uint64_t gblocks = (plan.rec_slots + 2047) / 2048;
+    const uint64_t gblocks = (plan.rec_slots + RC_SPAN - 1) / RC_SPAN;
     if (g.philox)
         launch_scatter<true, true, true, TT>(rg, B, sm_scatter, ss);
     else if (w1)
@@ -1224,7 +1228,7 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
             rg.kc = c1 - c0;
             rg.ntiles = (rg.kc + plan.tile - 1) / plan.tile;
             if ((e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st)) != cudaSuccess) return e;
-            const unsigned gblocks = static_cast<unsigned>((plan.rec_slots + 2047) / 2048);
+            const unsigned gblocks = static_cast<unsigned>((plan.rec_slots + RC_SPAN - 1) / RC_SPAN);
             const uint64_t span = static_cast<uint64_t>(K5_THREADS);
             const unsigned dblocks = static_cast<unsigned>(
                 umin64((rg.kc + span - 1) / span, static_cast<uint64_t>(sm_count()) * 8));
