@@ -659,6 +659,137 @@ __device__ __forceinline__ int carry_chain_pos(const double* in, double* out, in
     return v * B;
 }
 
+// K2a / K2c for a few blocks (CompSumPos): one CTA per 2048-block whose warps
+// run the parts of the block's chain concurrently, chunk-pipelined like
+// k_scan_carry_split -- warp 0 loads chunk c+1 and runs the hi chain of
+// chunk c (T[k] = hi = hi + x[k]), warp 1 the error terms of chunk c-1 (all
+// lanes), warp 2 the lo chain of chunk c-2 (L[k] = lo after the add), warp 3
+// the run's values T[k] + L[k] of chunk c-3 (pass 3, coalesced stores).
+// Pass 3 starts from run.add(carry[b]), which leaves (hi, lo) = (carry, 0)
+// exactly.  Bit-identical to the single-lane chain; worth it when the chains
+// are few enough that their latency is the kernel's time.
+constexpr int K2P_C = 256;  // elements per chunk
+template <bool PASS3>
+__global__ void __launch_bounds__(128)
+k_scan_blocks_split(const double* __restrict__ lw, const double* __restrict__ hw,
+                    double* __restrict__ lpre, double* __restrict__ hpre, const DevScalars* sc,
+                    double* __restrict__ totals, const double* __restrict__ carries) {
+    __shared__ __align__(16) double X[3][K2P_C];
+    __shared__ __align__(16) double T[4][K2P_C];
+    __shared__ __align__(16) double E[2][K2P_C];
+    __shared__ __align__(16) double Lo[2][K2P_C];
+    __shared__ double hin[4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t b = blockIdx.x;
+    const double* src;
+    double* dst;
+    int len;
+    if (b < nbl) {
+        src = lw + b * SCAN_BLOCK;
+        dst = lpre + 1 + b * SCAN_BLOCK;
+        len = static_cast<int>(umin64(SCAN_BLOCK, nl - b * SCAN_BLOCK));
+    } else if (b - nbl < nbh) {
+        const uint64_t hb = b - nbl;
+        src = hw + hb * SCAN_BLOCK;
+        dst = hpre + 1 + hb * SCAN_BLOCK;
+        len = static_cast<int>(umin64(SCAN_BLOCK, nh - hb * SCAN_BLOCK));
+    } else {
+        return;
+    }
+    const int nch = (len + K2P_C - 1) / K2P_C;
+    auto cnt_of = [&](int c) { return min(K2P_C, len - c * K2P_C); };
+    auto load = [&](int c) {
+        if (c < nch) {
+            const int cnt = cnt_of(c);
+            for (int i = lane; i < cnt; i += 32) cp_async8(&X[c % 3][i], src + c * K2P_C + i);
+        }
+        cp_async_commit();
+    };
+    auto h_at = [&](int c, int k) { return k ? T[c % 4][k - 1] : hin[c % 4]; };
+    double hi = PASS3 ? carries[b] : 0.0, lo = 0.0;  // run.add(carry[b]) = {carry, 0}
+    if (warp == 0) {
+        load(0);
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    for (int it = 0; it < nch + 3; ++it) {
+        if (warp == 0) {
+            load(it + 1);
+            const int c = it;
+            if (c < nch && lane == 0) {
+                const int cnt = cnt_of(c);
+                hin[c % 4] = hi;
+                int k = 0;
+                for (; k + 16 <= cnt; k += 16) {
+                    double x[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) x[u] = X[c % 3][k + u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        hi = hi + x[u];
+                        x[u] = hi;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) T[c % 4][k + u] = x[u];
+                }
+                for (; k < cnt; ++k) {
+                    hi = hi + X[c % 3][k];
+                    T[c % 4][k] = hi;
+                }
+            }
+            cp_async_wait<0>();
+        } else if (warp == 1) {
+            const int c = it - 1;
+            if (c >= 0 && c < nch) {
+                const int cnt = cnt_of(c);
+                for (int k = lane; k < cnt; k += 32) {
+                    const double h = h_at(c, k), x = X[c % 3][k];
+                    const bool big = h >= x;  // CompSumPos::add
+                    const double a = big ? h : x, bb = big ? x : h;
+                    E[c % 2][k] = (a - T[c % 4][k]) + bb;
+                }
+            }
+        } else if (warp == 2) {
+            const int c = it - 2;
+            if (c >= 0 && c < nch && lane == 0) {
+                const int cnt = cnt_of(c);
+                int k = 0;
+                for (; k + 16 <= cnt; k += 16) {
+                    double e[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) e[u] = E[c % 2][k + u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        lo = lo + e[u];
+                        e[u] = lo;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) Lo[c % 2][k + u] = e[u];
+                }
+                for (; k < cnt; ++k) {
+                    lo = lo + E[c % 2][k];
+                    Lo[c % 2][k] = lo;
+                }
+            }
+        } else if (PASS3) {
+            const int c = it - 3;
+            if (c >= 0 && c < nch) {
+                const int cnt = cnt_of(c);
+                for (int k = lane; k < cnt; k += 32)
+                    dst[c * K2P_C + k] = T[c % 4][k] + Lo[c % 2][k];  // run.value(), parallel.hpp:127
+            }
+        }
+        __syncthreads();
+    }
+    if (!PASS3 && warp == 2 && lane == 0 && len > 0) {
+        const int c = nch - 1;  // the last total's hi is in T, its lo in this lane
+        totals[b] = T[c % 4][cnt_of(c) - 1] + lo;  // carry[b] = local.value(), parallel.hpp:114
+    }
+}
+
 // K2b for CompSumPos, split over warps: one CTA per list, whose warps run the
 // parts of the compensated chain concurrently on different schedulers, chunk
 // by chunk (a CTA barrier between steps):
@@ -1310,6 +1441,13 @@ cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStrea
     return cudaGetLastError();
 }
 
+// Block count up to which K2a/K2c split each chain over warps
+// (k_scan_blocks_split; WRS_B200_K2_SPLIT_MAX: experiments).
+static uint64_t k2_split_max_blocks() {
+    const char* e = std::getenv("WRS_B200_K2_SPLIT_MAX");
+    return e ? std::strtoull(e, nullptr, 10) : 1536;  // measured: better up to 2^21 items, worse at 2^22
+}
+
 // Chains per warp of k_scan_blocks_direct (WRS_B200_K2_LPW: experiments).
 static int k2_direct_lpw(uint64_t nblocks) {
     if (const char* e = std::getenv("WRS_B200_K2_LPW")) {
@@ -1362,11 +1500,16 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     const bool pos = total < 1e300;
     // few chains per SM: their latency sets the time, so the leaner direct form
     const bool direct = n <= k2_direct_max();
+    // a few blocks (n up to ~3e6 items): each chain split over four warps
+    const bool split = pos && nblocks <= k2_split_max_blocks();
     const int lpw = k2_direct_lpw(nblocks);
     const unsigned k2d_grid = static_cast<unsigned>((nblocks + 2 * lpw - 1) / (2 * lpw));
 #define K2_LAUNCH(PASS3)                                                                          \
     do {                                                                                          \
-        if (direct && pos)                                                                        \
+        if (split)                                                                                \
+            k_scan_blocks_split<PASS3><<<static_cast<unsigned>(nblocks), 128, 0, st>>>(           \
+                ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
+        else if (direct && pos)                                                                   \
             k_scan_blocks_direct<PASS3, CompSumPos><<<k2d_grid, 64, 0, st>>>(                     \
                 ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries, lpw);               \
         else if (direct)                                                                          \

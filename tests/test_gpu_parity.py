@@ -94,11 +94,12 @@ def test_golden_medium_generators_and_tables():
 
 # ---- per-stage parity ------------------------------------------------------------
 
-@pytest.mark.parametrize("k2", ["direct", "direct-lpw1", "direct-lpw32", "staged"])
+@pytest.mark.parametrize("k2", ["split", "direct", "direct-lpw1", "direct-lpw32", "staged"])
 def test_stages_bit_exact(P, k2, monkeypatch):
-    # K2a/K2c have two forms (register-direct for small tables, with 1..32
-    # chains per warp, and smem-staged above 2^25 items); all must produce
-    # the same prefix arrays
+    # K2a/K2c have three forms (chains split over warps for a few blocks,
+    # register-direct for small tables with 1..32 chains per warp, and
+    # smem-staged above 2^25 items); all must produce the same prefix arrays
+    monkeypatch.setenv("WRS_B200_K2_SPLIT_MAX", str(2**62 if k2 == "split" else 0))
     monkeypatch.setenv("WRS_B200_K2_DIRECT_MAX", str(0 if k2 == "staged" else 2**62))
     if "lpw" in k2:
         monkeypatch.setenv("WRS_B200_K2_LPW", k2.split("lpw")[1])
