@@ -28,6 +28,7 @@
 // No stage needs a host round trip: counts live in DevScalars and every grid
 // is sized from upper bounds.
 #include <atomic>
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 #include <cstdio>
@@ -1093,7 +1094,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
     if (nh == 0) return;  // all items tie with the mean: K4b fills (alias.hpp:288-297)
     const double wn = sc->wn;
 
-    const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * K4_WARPS + wq) * 32 + lane;
+    const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + wq) * 32 + lane;
     uint64_t i = 0, lhi = 0, j = 0, hhi = 0;
     int state = ST_DONE;
     CompSum rem{0.0, 0.0};
@@ -1471,7 +1472,14 @@ static uint64_t k2_direct_max() {
 cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
                              Bucket* d_b, Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
     const int k1_smem = K1_TILE * 10;
-    const int k4_smem = K4_WARPS * static_cast<int>(sizeof(K4Smem));
+    // warps per K4a CTA: 11 fill an SM's shared memory; with fewer jobs than
+    // 11 warps on every SM, smaller CTAs spread the sequential chains over
+    // more SMs (a lone chain is issue-latency bound, so it runs faster with a
+    // scheduler to itself)
+    const uint64_t k4_warps_total = (P + 31) / 32;
+    const int k4_warps = static_cast<int>(std::min<uint64_t>(
+        K4_WARPS, std::max<uint64_t>(1, (k4_warps_total + 147) / 148)));
+    const int k4_smem = k4_warps * static_cast<int>(sizeof(K4Smem));
     // per-device attribute; cheap enough to set on every build
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
     cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
@@ -1481,7 +1489,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
     const unsigned k2_grid = static_cast<unsigned>((nblocks + K2_WARPS * 32 - 1) / (K2_WARPS * 32));
     const unsigned k3_grid = static_cast<unsigned>((P + 255) / 256);
-    const unsigned k4_grid = static_cast<unsigned>((P + K4_WARPS * 32 - 1) / (K4_WARPS * 32));
+    const unsigned k4_grid = static_cast<unsigned>((P + k4_warps * 32 - 1) / (k4_warps * 32));
     cudaError_t e;
 #define REC(i)                                          \
     do {                                                \
@@ -1535,7 +1543,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
                                      ws.split_s);
     REC(5);
-    k_pack<<<k4_grid, K4_WARPS * 32, k4_smem, st>>>(P, ws.sc, ws.lw, ws.hidx, ws.hw, ws.split_l,
+    k_pack<<<k4_grid, k4_warps * 32, k4_smem, st>>>(P, ws.sc, ws.lw, ws.hidx, ws.hw, ws.split_l,
                                                     ws.split_h, ws.split_s, ws.lalias, ws.hshare,
                                                     ws.halias);
     REC(6);
