@@ -587,78 +587,11 @@ k_scan_blocks_direct(const double* __restrict__ lw, const double* __restrict__ h
 
 // ===========================================================================
 // K2b: serial carry chain over the block totals (parallel.hpp:116-121)
-//   One lane per list runs the inherently sequential Neumaier chain; the rest
-//   of the warp streams the totals into shared memory ahead of it.  The loop
-//   is unrolled so smem loads and carry stores leave the dependent DADD chain.
+//   CompSumPos (W < 1e300): k_scan_carry_split, the chain's parts on separate
+//   warps.  Guarded CompSum: k_scan_carry, one lane per list runs the chain
+//   while the rest of the warp streams the totals into shared memory.
 // ===========================================================================
 constexpr int K2B_CHUNK = 1024;
-constexpr int K2B_B = 4;  // adds per software-pipeline stage
-
-// The carry chain for CompSumPos, software-pipelined by hand over blocks of
-// B totals.  Block v goes through three stages in consecutive steps: the hi
-// chain (t = hi + x), the error terms e = (max - t) + min (independent of
-// each other), and the lo chain (lo += e) with the output hi + lo of the
-// state before each add.  Step v runs hi(v), e(v-1), lo(v-2) interleaved add
-// by add, so the in-order warp always has independent FP64 work between the
-// dependent DADDs of each chain.  Exactly the additions of CompSumPos::add, in
-// the same order per chain.  Register sets rotate mod 3 (compile-time via an
-// unroll by 3).  Returns the number of totals consumed; the caller finishes.
-struct ChainRegs {
-    double X[3][K2B_B], H[3][K2B_B], T[3][K2B_B], E[3][K2B_B];
-};
-template <int SH, int SE, int SL, bool DH, bool DE, bool DL>
-__device__ __forceinline__ void chain_step(const double* in, double* out, int v, double& hi,
-                                           double& lo, ChainRegs& R) {
-    constexpr int B = K2B_B;
-    if (DH) {
-#pragma unroll
-        for (int u = 0; u < B; ++u) R.X[SH][u] = in[v * B + u];
-    }
-    double lb[B];
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-        if (DH) {
-            R.H[SH][u] = hi;
-            R.T[SH][u] = hi + R.X[SH][u];
-            hi = R.T[SH][u];
-        }
-        if (DE) {
-            const bool big = R.H[SE][u] >= R.X[SE][u];
-            const double a = big ? R.H[SE][u] : R.X[SE][u], b = big ? R.X[SE][u] : R.H[SE][u];
-            R.E[SE][u] = (a - R.T[SE][u]) + b;
-        }
-        if (DL) {
-            lb[u] = lo;
-            lo = lo + R.E[SL][u];
-        }
-    }
-    if (DL) {
-#pragma unroll
-        for (int u = 0; u < B; ++u) out[(v - 2) * B + u] = R.H[SL][u] + lb[u];  // acc.value()
-    }
-}
-__device__ __forceinline__ int carry_chain_pos(const double* in, double* out, int cnt,
-                                               CompSumPos& acc) {
-    constexpr int B = K2B_B;
-    const int nblk = cnt / B;
-    if (nblk < 5) return 0;
-    double hi = acc.hi, lo = acc.lo;
-    ChainRegs R;
-    chain_step<0, 0, 0, true, false, false>(in, out, 0, hi, lo, R);  // hi(0)
-    chain_step<1, 0, 0, true, true, false>(in, out, 1, hi, lo, R);   // hi(1), e(0)
-    int v = 2;
-    for (; v + 3 <= nblk; v += 3) {
-        chain_step<2, 1, 0, true, true, true>(in, out, v, hi, lo, R);
-        chain_step<0, 2, 1, true, true, true>(in, out, v + 1, hi, lo, R);
-        chain_step<1, 0, 2, true, true, true>(in, out, v + 2, hi, lo, R);
-    }
-    // v = 2 mod 3: block v-2 (set 0) waits for lo, block v-1 (set 1) for e, lo
-    chain_step<0, 1, 0, false, true, true>(in, out, v, hi, lo, R);      // e(v-1), lo(v-2)
-    chain_step<0, 0, 1, false, false, true>(in, out, v + 1, hi, lo, R);  // lo(v-1)
-    acc.hi = hi;
-    acc.lo = lo;
-    return v * B;
-}
 
 // K2a / K2c for a few blocks (CompSumPos): one CTA per 2048-block whose warps
 // run the parts of the block's chain concurrently, chunk-pipelined like
@@ -972,9 +905,6 @@ k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* ca
             double* out = dst + c * K2B_CHUNK;
             const double* in = buf[bsel];
             int i = 0;
-            if constexpr (std::is_same<CS, CompSumPos>::value) {
-                i = carry_chain_pos(in, out, cnt, acc);
-            }
             for (; i + 16 <= cnt; i += 16) {
                 double t[16], hs[16], ls[16];
 #pragma unroll
