@@ -993,8 +993,17 @@ k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__
 // 3052 warps) the 1628 resident warps run the pack in 2 rounds; 32-step
 // phases (672 B per lane) allowed only 10 warps per SM, i.e. 3 rounds, the
 // last one with 6% of the warps.
-constexpr int K4_S = 30;      // steps per phase (= max items consumed per list)
-constexpr int K4_WARPS = 11;
+// measured at n = 1e8: S = 30 / 11 warps 0.98 ms (two rounds of 1628 warps),
+// S = 20 / 15 warps 1.51 ms, S = 14 / 21 warps (one round) 2.04 ms: the
+// per-phase staging and flush outweigh the extra warps
+#ifndef K4_S_DEF
+#define K4_S_DEF 30
+#endif
+#ifndef K4_WARPS_DEF
+#define K4_WARPS_DEF 11
+#endif
+constexpr int K4_S = K4_S_DEF;          // steps per phase (= max items consumed per list)
+constexpr int K4_WARPS = K4_WARPS_DEF;  // warps per CTA (windows fill an SM's shared memory)
 constexpr int K4_LW = K4_S + 1;     // light window row stride (odd -> no bank conflicts)
 constexpr int K4_HWIN = K4_S + 2;   // heavy window entries (S + 1 lookahead)
 constexpr int K4_HW = K4_S + 3;     // heavy window row stride (odd -> no bank conflicts)
