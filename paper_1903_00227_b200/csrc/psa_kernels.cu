@@ -356,6 +356,10 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
 constexpr int SCAN_BLOCK = 2048;  // kScanBlock, parallel.hpp:60
 constexpr int K2_WARPS = 2;
 constexpr int K2_C = 32;          // chunk of each block staged per step
+#ifndef K2_ROW_UNROLL
+#define K2_ROW_UNROLL 4
+#endif
+constexpr int K2_ROW_U = K2_ROW_UNROLL;  // rows per unrolled step of the staging loops
 
 struct K2Lane {
     const double* src;
@@ -399,7 +403,7 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
 
     const int nchunks = (maxlen + K2_C - 1) / K2_C;
     auto load_chunk = [&](int c, int buf) {
-#pragma unroll 4
+#pragma unroll K2_ROW_U
         for (int r = 0; r < 32; ++r) {
             const K2Lane L = lanes[wq][r];
             const int e = c * K2_C + lane;
@@ -448,7 +452,7 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
         }
         __syncwarp();
         if (PASS3) {
-#pragma unroll 4
+#pragma unroll K2_ROW_U
             for (int r = 0; r < 32; ++r) {
                 const K2Lane L = lanes[wq][r];
                 const int e = c * K2_C + lane;
@@ -1213,6 +1217,10 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
 #define K4B_SMEM_KB 40
 #endif
 constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // staging budget: 5 CTAs per SM at 40 KB
+#ifndef K4B_ROW_UNROLL
+#define K4B_ROW_UNROLL 4
+#endif
+constexpr int K4B_ROW_U = K4B_ROW_UNROLL;
 __global__ void __launch_bounds__(K1_THREADS)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
            const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lalias,
@@ -1256,7 +1264,7 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     }
     __syncthreads();
     const unsigned lt = lanemask_lt();
-#pragma unroll 4
+#pragma unroll K4B_ROW_U
     for (int r = 0; r < K1_ROWS; ++r) {
         const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
         if (gi >= n) continue;
