@@ -1009,7 +1009,11 @@ k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__
 #ifndef K4_ROW_UNROLL
 #define K4_ROW_UNROLL 32  // full: 0.96 vs 0.98 ms at unroll 8
 #endif
-constexpr int K4_ROW_U = K4_ROW_UNROLL;  // rows per unrolled step of the staging / flush loops
+constexpr int K4_ROW_U = K4_ROW_UNROLL;
+#ifndef K4_STEP_UNROLL
+#define K4_STEP_UNROLL 1  // measured 0.945 ms vs 0.959 at 2, 0.963 at 4
+#endif
+constexpr int K4_STEP_U = K4_STEP_UNROLL;  // steps per unrolled step of the sweep loops  // rows per unrolled step of the staging / flush loops
 constexpr int K4_S = K4_S_DEF;          // steps per phase (= max items consumed per list)
 constexpr int K4_WARPS = K4_WARPS_DEF;  // warps per CTA (windows fill an SM's shared memory)
 constexpr int K4_LW = K4_S + 1;     // light window row stride (odd -> no bank conflicts)
@@ -1121,7 +1125,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
         // is the main loop's body alone (alias.hpp:175-189), identical values.
         const bool fast = __all_sync(0xffffffffu, state == ST_MAIN && lrem == K4_S + 1 &&
                                                       hrem == K4_S + 2 && hlast == K4_S + 2);
-#pragma unroll 2
+#pragma unroll K4_STEP_U
         for (int step = 0; fast && step < K4_S; ++step) {
             const double v = rem.value();
             const bool gt = v > wn;
@@ -1139,7 +1143,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
                 hNextW = S.hw[lane][hj + 1];
             }
         }
-#pragma unroll 2
+#pragma unroll K4_STEP_U
         for (int step = 0; !fast && step < K4_S; ++step) {
             const double v = rem.value();
             const bool gt = v > wn;
