@@ -318,9 +318,10 @@ __device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t 
 }
 
 // RB: draws -> region slabs.  Each thread computes 16 draws' buckets and
-// claims a rank inside its region with a shared-memory atomic; a warp scan
-// turns the region counts into tile-local run starts; the (draw, bucket)
-// records are staged in shared memory in region order and each run is then
+// counts them per region (shared-memory atomics); a warp scan turns the counts
+// into tile-local run starts while other warps claim the runs' slab space; each
+// draw then takes a staging slot from its region's fill cursor, the (draw,
+// bucket) records are staged in shared memory in region order, and each run is
 // written to its slab as one contiguous block.  The tile slot of every draw
 // is recorded (q order) for RD, so the (non-deterministic) order inside a run
 // never needs to be reproduced.
