@@ -11,11 +11,16 @@
 //                      (light ids stay implicit: K4b recovers them).
 //   K2a k_scan_blocks  prefix_sums pass 1 (parallel.hpp:110-115): Neumaier
 //                      total of every 2048-element block, thread per block,
-//                      warp-transposed through shared memory.
-//   K2b k_scan_carry   pass 2 (:116-121): serial Neumaier chain of the block
-//                      totals, light and heavy lists in parallel.
+//                      warp-transposed through shared memory (smaller tables:
+//                      k_scan_blocks_direct, register-direct loads, or
+//                      k_scan_blocks_split, each chain split over warps).
+//   K2b k_scan_carry_split  pass 2 (:116-121): serial Neumaier chain of the
+//                      block totals, light and heavy lists in parallel, the
+//                      chain's hi / error / lo parts on separate warps
+//                      (k_scan_carry: the guarded form, W >= 1e300).
 //   K2c k_scan_blocks  pass 3 (:122-129): block chains seeded with the carry,
-//                      writing the exclusive prefix arrays (alias.hpp:82-95).
+//                      writing the exclusive prefix arrays (alias.hpp:82-95);
+//                      same three forms as K2a.
 //   K3  k_split        psa_split binary searches (alias.hpp:122-149), the
 //                      same probe sequence, one thread per split.
 //   K4a k_pack         psa_pack (alias.hpp:160-209), one lane per job, run in
