@@ -23,6 +23,11 @@ extern "C" {
  * reference at this same count. */
 WRS_API uint64_t wrs_b200_default_jobs(uint64_t n);
 
+/* The library keeps freed device buffers for reuse (at most WRS_B200_CACHE_MB,
+ * default 8192 MB, per process).  Returns every cached buffer to the driver
+ * and the number of bytes released. */
+WRS_API uint64_t wrs_b200_release_cache(void);
+
 /* Weights already in device memory of the current CUDA device.  copy != 0
  * duplicates them; copy == 0 borrows d_w (caller keeps it alive and
  * unchanged until every handle built from it is freed). */

@@ -294,6 +294,11 @@ class Ref:
         lib.ref_table_free.argtypes = [vp]
         lib.ref_table_buckets.argtypes = [vp, vp, C.POINTER(f64)]
         lib.ref_table_sample_many.argtypes = [vp, u64, u64, C.c_uint, vp]
+        lib.ref_wt_new.restype = vp
+        lib.ref_wt_new.argtypes = [vp, u64]
+        lib.ref_wt_free.argtypes = [vp]
+        lib.ref_table_from_wt.restype = vp
+        lib.ref_table_from_wt.argtypes = [vp, C.c_uint]
         lib.ref_outbuf_new.restype = vp
         lib.ref_outbuf_new.argtypes = [u64]
         lib.ref_outbuf_free.argtypes = [vp]

@@ -207,6 +207,26 @@ void ref_table_sample_many(void* h, uint64_t seed, uint64_t k, unsigned workers,
     std::memcpy(out, buf.data(), k * sizeof(uint32_t));
 }
 
+/* The CPU baseline's pieces (BASELINE.md "CPU baseline plan"): the
+ * WeightTable is made outside the timed region, AliasTable(wt, psa, T) is
+ * timed alone (bucket allocation and first touch included, alias.hpp:251). */
+void* ref_wt_new(const double* w, uint64_t n) {
+    try {
+        return new wrs::WeightTable(table_of(w, n));
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+void ref_wt_free(void* wt) { delete static_cast<wrs::WeightTable*>(wt); }
+void* ref_table_from_wt(const void* wt, unsigned workers) {
+    try {
+        return new wrs::AliasTable(*static_cast<const wrs::WeightTable*>(wt),
+                                   wrs::AliasTable::Build::psa, workers);
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+
 /* Time-honest variant for the CPU baseline: the caller's vector is reused
  * across calls, as the reference's own benchmark does (alias.hpp:271-273). */
 void* ref_outbuf_new(uint64_t k) {

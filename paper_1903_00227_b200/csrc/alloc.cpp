@@ -7,11 +7,14 @@
 // time.  Freed blocks are kept per (device, size) and handed out again for an
 // allocation of exactly that size.  A block is cached only after the device
 // is idle (cudaDeviceSynchronize), so no in-flight work can still touch it.
-// Cached bytes are capped; an allocation that fails for lack of memory
-// returns every cached block of its device and retries.
+// Cached bytes are capped (WRS_B200_CACHE_MB, default 8 GB per process);
+// an allocation that fails for lack of memory returns every cached block of
+// its device and retries, and wrs_b200_release_cache() hands every cached
+// block back to the driver (e.g. before a co-resident framework allocates).
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -28,11 +31,15 @@ struct Cache {
     std::multimap<std::pair<int, size_t>, void*> free_blocks;
     std::unordered_map<void*, std::pair<int, size_t>> live;
     size_t cached = 0;
-    static constexpr size_t kLimit = size_t{32} << 30;  // bytes kept per process
+    const size_t limit = [] {
+        const char* e = std::getenv("WRS_B200_CACHE_MB");
+        return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) << 20 : size_t{8} << 30;
+    }();
 
+    // dev < 0: every device
     void release_device(int dev) {
         for (auto it = free_blocks.begin(); it != free_blocks.end();) {
-            if (it->first.first == dev) {
+            if (dev < 0 || it->first.first == dev) {
                 cudaFree(it->second);
                 cached -= it->first.second;
                 it = free_blocks.erase(it);
@@ -89,13 +96,24 @@ void dev_free(void* p) {
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != key.first) cudaSetDevice(key.first);
-    if (c.cached + key.second <= Cache::kLimit && cudaDeviceSynchronize() == cudaSuccess) {
+    if (c.cached + key.second <= c.limit && cudaDeviceSynchronize() == cudaSuccess) {
         c.free_blocks.insert({key, p});
         c.cached += key.second;
     } else {
         cudaFree(p);
     }
     if (cur != key.first) cudaSetDevice(cur);
+}
+
+size_t release_cache() {
+    Cache& c = cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    const size_t had = c.cached;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    c.release_device(-1);
+    cudaSetDevice(cur);
+    return had;
 }
 
 }  // namespace wrsb

@@ -13,6 +13,7 @@
 #include <thread>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -229,6 +230,14 @@ std::shared_ptr<WeightsData> powerlaw_device(uint64_t n, double s, uint64_t seed
     }
     finalize_weights(*wd, "");
     return wd;
+}
+
+// WRS_B200_PSA_EXACT=1 makes "psa" honour `workers` as the job count, so an
+// unmodified reference client gets the reference's table (and draw stream)
+// byte for byte without switching to "psa-exact".
+bool psa_exact_env() {
+    const char* e = std::getenv("WRS_B200_PSA_EXACT");
+    return e && e[0] == '1';
 }
 
 }  // namespace
@@ -615,7 +624,9 @@ wrs_status wrs_sampler_build(const wrs_weights* w, const char* algo, unsigned wo
     return guarded([&]() -> wrs_status {
         const std::string name = algo;
         uint64_t P;
-        if (name == "psa")
+        if (name == "psa" && psa_exact_env())
+            P = std::max(1u, workers);  // WRS_B200_PSA_EXACT=1: the reference's own job count
+        else if (name == "psa")
             P = wrsb::default_jobs(w->data->n);
         else if (name == "psa-exact")
             P = std::max(1u, workers);
@@ -707,6 +718,8 @@ wrs_status wrs_verify(const char*, uint64_t, int) { return not_in_path("wrs_veri
 
 // ---- B200 extensions -------------------------------------------------------------
 uint64_t wrs_b200_default_jobs(uint64_t n) { return wrsb::default_jobs(n); }
+
+uint64_t wrs_b200_release_cache(void) { return wrsb::release_cache(); }
 
 wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
                                         wrs_weights** out) {

@@ -13,6 +13,8 @@ namespace wrsb {
 // Caching device allocator for the library's large buffers (alloc.cpp).
 cudaError_t dev_malloc(void** p, size_t bytes);
 void dev_free(void* p);
+// Returns every cached block to the driver; the bytes released.
+size_t release_cache();
 
 // PSA job count used by algo "psa": one job = one thread's sequential pack
 // chain, so P sets the build's parallelism and the job length its latency.

@@ -32,7 +32,6 @@
 //
 // No stage needs a host round trip: counts live in DevScalars and every grid
 // is sized from upper bounds.
-#include <atomic>
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -1373,23 +1372,21 @@ void workspace_free(Workspace& ws) {
     ws = Workspace{};
 }
 
-// DevScalars is tiny: one async H2D from a pinned per-device staging slot.
+// DevScalars of a build, written by a one-thread kernel: total and wn travel
+// as launch parameters (captured at launch), so no host staging buffer can be
+// reused while a copy from it is still pending, however many builds are in
+// flight.
+__global__ void k_reset_scalars(DevScalars* sc, double total, double wn) {
+    DevScalars v{};
+    v.bad_index = ~0ull;
+    v.total = total;
+    v.wn = wn;
+    *sc = v;
+}
+
 static cudaError_t reset_scalars(Workspace& ws, cudaStream_t st, double total, double wn) {
-    constexpr int kSlots = 64;  // ring of pinned slots; a slot is reused 64 builds later
-    static DevScalars* pinned = [] {
-        DevScalars* p = nullptr;
-        if (cudaMallocHost(reinterpret_cast<void**>(&p), kSlots * sizeof(DevScalars)) != cudaSuccess)
-            return static_cast<DevScalars*>(nullptr);
-        return p;
-    }();
-    static std::atomic<unsigned> next{0};
-    if (!pinned) return cudaErrorMemoryAllocation;
-    DevScalars* slot = pinned + (next.fetch_add(1) % kSlots);
-    *slot = DevScalars{};
-    slot->bad_index = ~0ull;
-    slot->total = total;
-    slot->wn = wn;
-    return cudaMemcpyAsync(ws.sc, slot, sizeof(DevScalars), cudaMemcpyHostToDevice, st);
+    k_reset_scalars<<<1, 1, 0, st>>>(ws.sc, total, wn);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_total(const double* d_w, uint64_t n, Workspace& ws, cudaStream_t st) {

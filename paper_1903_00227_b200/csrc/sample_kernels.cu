@@ -437,6 +437,9 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
                 if (base + c <= rg.cap) {
                     g = reg * rg.cap + base;
                 } else {
+                    // the slab keeps only the runs claimed below this one:
+                    // positions from here on are never written
+                    atomicMin(&cursor[nreg + 1 + reg], base);
                     const uint32_t ob = atomicAdd(&cursor[nreg], c);
                     if (ob + c > rg.ov_cap) atomicOr(overflow, 1u);
                     g = nreg * rg.cap + (ob + c <= rg.ov_cap ? ob : 0);
@@ -481,6 +484,18 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     }
 }
 
+// End of the written records of slab `slab` (nreg = the overflow slab):
+// cursor[0, nreg) are the region fill cursors, cursor[nreg] the overflow
+// slab's, cursor[nreg + 1 + r] the base of region r's first run that did not
+// fit (~0 if none; every run claimed below it was written).
+__device__ __forceinline__ uint64_t slab_valid_end(const RegionGeom& rg, const uint32_t* cursor,
+                                                   uint32_t slab) {
+    const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
+    if (slab < rg.nreg)
+        return slab0 + umin64(umin64(cursor[slab], rg.cap), cursor[rg.nreg + 1 + slab]);
+    return slab0 + umin64(cursor[rg.nreg], rg.ov_cap);
+}
+
 // RC: slab by slab, the coin flip of every record against its bucket.  One
 // contiguous run of RC_SPAN slab positions per CTA, so the resident CTAs of the
 // GPU sweep the table region by region; table loads are marked evict-last,
@@ -488,12 +503,12 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
 template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(256, RC_MIN_CTAS)
 k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
-                const uint2* __restrict__ rec, uint32_t* __restrict__ res) {
+                const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
+                uint32_t* __restrict__ res) {
+    if (*overflow) return;  // the overflow slab overflowed: RD recomputes the chunk directly
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
     const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);  // nreg = overflow slab
-    const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
-    const uint64_t valid_end =
-        slab0 + (slab < rg.nreg ? umin64(cursor[slab], rg.cap) : umin64(cursor[rg.nreg], rg.ov_cap));
+    const uint64_t valid_end = slab_valid_end(rg, cursor, slab);
     if (p0 >= valid_end) return;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
@@ -648,9 +663,7 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
     if (*overflow) return;  // k_count_direct<.., true> recounts the chunk
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
     const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);
-    const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
-    const uint64_t valid_end =
-        slab0 + (slab < rg.nreg ? umin64(cursor[slab], rg.cap) : umin64(cursor[rg.nreg], rg.ov_cap));
+    const uint64_t valid_end = slab_valid_end(rg, cursor, slab);
     if (p0 >= valid_end) return;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
@@ -973,6 +986,9 @@ static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     auto round2k = [](uint64_t x) { return static_cast<uint32_t>((x + RC_SPAN - 1) / RC_SPAN * RC_SPAN); };
     p.rg.cap = round2k(static_cast<uint64_t>(cap < static_cast<double>(chunk) ? cap : chunk) + p.tile);
     p.rg.ov_cap = round2k(chunk / 64 + 8 * p.tile);
+    // tests: shrink the slabs to force the redirect / overflow paths
+    if (const char* e = getenv("WRS_B200_TEST_SLAB_CAP")) p.rg.cap = round2k(strtoull(e, nullptr, 10));
+    if (const char* e = getenv("WRS_B200_TEST_OV_CAP")) p.rg.ov_cap = round2k(strtoull(e, nullptr, 10));
     p.rec_slots = static_cast<uint64_t>(p.rg.nreg) * p.rg.cap + p.rg.ov_cap;
     return p;
 }
@@ -995,6 +1011,14 @@ struct RegionBuffers {
     unsigned* overflow;
 };
 
+// fill cursors and the overflow flag to 0, the failed-run bases to ~0
+static cudaError_t reset_cursors(const RegionGeom& rg, const RegionBuffers& B, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 1) * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(B.cursor + rg.nreg + 1, 0xff, rg.nreg * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(B.overflow, 0, 4, st);
+    return e;
+}
+
 static uint64_t region_bytes(const RegionPlan& p, uint64_t chunk, RegionBuffers* b, void* base) {
     const uint64_t ntiles = (chunk + p.tile - 1) / p.tile;
     uint64_t off = 0;
@@ -1007,14 +1031,14 @@ static uint64_t region_bytes(const RegionPlan& p, uint64_t chunk, RegionBuffers*
     char* res = take(p.rec_slots * sizeof(uint32_t));
     char* slot = take(chunk * sizeof(uint16_t));
     char* runs = take(ntiles * p.rg.nreg * sizeof(RunInfo));
-    char* cur = take((p.rg.nreg + 1) * 4 + 4);
+    char* cur = take((2 * p.rg.nreg + 1) * 4 + 4);
     if (b) {
         b->rec = reinterpret_cast<uint2*>(rec);
         b->res = reinterpret_cast<uint32_t*>(res);
         b->slot_of = reinterpret_cast<uint16_t*>(slot);
         b->runs = reinterpret_cast<RunInfo*>(runs);
         b->cursor = reinterpret_cast<uint32_t*>(cur);
-        b->overflow = reinterpret_cast<unsigned*>(cur) + p.rg.nreg + 1;
+        b->overflow = reinterpret_cast<unsigned*>(cur) + 2 * p.rg.nreg + 1;
     }
     return off;
 }
@@ -1066,7 +1090,7 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
     const int sm_unperm = static_cast<int>(plan.tile * sizeof(uint32_t));
     const bool w1 = g.W == 1;
     cudaStream_t ss = on_side ? side : st;
-    cudaError_t e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, ss);
+    cudaError_t e = reset_cursors(rg, B, ss);
     if (e != cudaSuccess) return e;
     const unsigned tiles = static_cast<unsigned>(rg.ntiles);
     const uint64_t gblocks = (plan.rec_slots + RC_SPAN - 1) / RC_SPAN;
@@ -1084,21 +1108,21 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
         cudaFuncSetAttribute(k_region_unpermute<true, true, TT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
         k_region_gather<true, true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.rec, B.res);
+            rg, d_b, B.cursor, B.overflow, B.rec, B.res);
         k_region_unpermute<true, true, TT><<<tiles, TT, sm_unperm, st>>>(
             rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
     } else if (w1) {
         cudaFuncSetAttribute(k_region_unpermute<true, false, TT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
         k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.rec, B.res);
+            rg, d_b, B.cursor, B.overflow, B.rec, B.res);
         k_region_unpermute<true, false, TT><<<tiles, TT, sm_unperm, st>>>(
             rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
     } else {
         cudaFuncSetAttribute(k_region_unpermute<false, false, TT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
         k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.rec, B.res);
+            rg, d_b, B.cursor, B.overflow, B.rec, B.res);
         k_region_unpermute<false, false, TT><<<tiles, TT, sm_unperm, st>>>(
             rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
     }
@@ -1228,7 +1252,7 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
             rg.q0 = c0;
             rg.kc = c1 - c0;
             rg.ntiles = (rg.kc + plan.tile - 1) / plan.tile;
-            if ((e = cudaMemsetAsync(B.cursor, 0, (rg.nreg + 2) * 4, st)) != cudaSuccess) return e;
+            if ((e = reset_cursors(rg, B, st)) != cudaSuccess) return e;
             const unsigned gblocks = static_cast<unsigned>((plan.rec_slots + RC_SPAN - 1) / RC_SPAN);
             const uint64_t span = static_cast<uint64_t>(K5_THREADS);
             const unsigned dblocks = static_cast<unsigned>(

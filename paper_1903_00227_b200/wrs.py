@@ -51,6 +51,7 @@ SIGNATURES = {
     "wrs_reservoir_free": (None, [vp]),
     "wrs_verify": (C.c_int, [C.c_char_p, u64, C.c_int]),
     "wrs_b200_default_jobs": (u64, [u64]),
+    "wrs_b200_release_cache": (u64, []),
     "wrs_b200_weights_from_device": (C.c_int, [vp, u64, C.c_int, C.POINTER(vp)]),
     "wrs_b200_weights_generate_range": (C.c_int, [C.c_char_p, f64, u64, u64, u64, u64,
                                                   C.POINTER(vp)]),
@@ -196,6 +197,14 @@ class Weights:
         obj = cls(h)
         obj._keepalive = tensor
         return obj
+
+    @classmethod
+    def from_device_ptr(cls, ptr: int, n: int, copy: bool = True) -> "Weights":
+        """B200 extension: n float64 weights at device address ptr (e.g. a
+        slice of another handle's device_ptr()); copy=False borrows them."""
+        h = vp()
+        _check(lib().wrs_b200_weights_from_device(vp(ptr), n, 1 if copy else 0, C.byref(h)))
+        return cls(h)
 
     def write(self, path: str) -> None:
         _check(lib().wrs_weights_write(self.h, os.fsencode(path)))
@@ -366,6 +375,11 @@ class Sampler:
             self.free()
         except Exception:
             pass
+
+
+def release_cache() -> int:
+    """wrs_b200_release_cache: return the library's cached device buffers."""
+    return int(lib().wrs_b200_release_cache())
 
 
 def set_timing(on: bool) -> None:

@@ -171,8 +171,98 @@ def two_level(R):
     np.savez_compressed(os.path.join(HERE, "two_level.npz"), **t)
 
 
+def default_jobs(n: int) -> int:
+    """wrs_b200_default_jobs (engine.h): the job count "psa" uses."""
+    j = 32
+    while j < 1024 and 2 * j <= n // 49152:
+        j *= 2
+    return max(1, -(-n // j))
+
+
+def large(R):
+    """Full-size pins (VERDICT r1 "next" #1): reference-build digests of
+    BASELINE configs[2]'s input generate_powerlaw(1e9, 1.0, 42)
+    (weight_file.hpp:42-54), its G-shard totals (two_level.hpp:33-51: each a
+    WeightTable over the contiguous block), the PSA tables of shards g = 0 and
+    g = 7 of G = 8 at several job counts (alias.hpp:411-419 via the detail::
+    pieces), and the configs[1] n = 1e8 uniform table at the job counts of
+    1024-, 512- and 2048-item jobs.  Needs ~40 GB of host memory and a few
+    minutes; writes psa_large.npz."""
+    m = {}
+    n = 10**9
+    w = R.generate_powerlaw(n, 1.0, 42)
+    m["pl1_1e9_s42/w_sha"] = sha(w)
+    m["pl1_1e9_s42/w_head"] = w[:16].copy()
+    m["pl1_1e9_s42/total"] = np.float64(R.pairwise_sum(w))
+    for G in (2, 4, 8):
+        block = -(-n // G)
+        m[f"pl1_1e9_s42/G{G}/totals"] = np.array(
+            [R.pairwise_sum(w[g * block:min(n, (g + 1) * block)]) for g in range(G)], np.float64)
+    block = -(-n // 8)
+    for g in (0, 7):
+        ws = np.ascontiguousarray(w[g * block:min(n, (g + 1) * block)])
+        m[f"pl1_1e9_s42/G8/g{g}/w_sha"] = sha(ws)
+        ns = ws.size
+        Ps = sorted({default_jobs(ns), -(-ns // 512), -(-ns // 2048)})
+        m[f"pl1_1e9_s42/G8/g{g}/jobs"] = np.array(Ps, np.uint64)
+        for P in Ps:
+            b, wn = R.psa_build_jobs(ws, P, 8)
+            m[f"pl1_1e9_s42/G8/g{g}/P{P}/buckets_sha"] = sha(b)
+            m[f"pl1_1e9_s42/G8/g{g}/P{P}/bucket_mean"] = np.float64(wn)
+            if P == default_jobs(ns):
+                masses = R.implied_masses(b, wn)
+                m[f"pl1_1e9_s42/G8/g{g}/P{P}/max_rel_err"] = np.float64(
+                    np.max(np.abs(masses - ws) / ws))
+                del masses
+            del b
+        del ws
+        print("shard", g, "done", flush=True)
+    del w
+    n = 10**8
+    w = R.generate_uniform(n, 42)
+    Ps = sorted({default_jobs(n), -(-n // 512), -(-n // 2048)})
+    m["uniform_1e8_s42/jobs"] = np.array(Ps, np.uint64)
+    for P in Ps:
+        b, wn = R.psa_build_jobs(w, P, 8)
+        m[f"uniform_1e8_s42/P{P}/buckets_sha"] = sha(b)
+        m[f"uniform_1e8_s42/P{P}/bucket_mean"] = np.float64(wn)
+        if P == default_jobs(n):
+            masses = R.implied_masses(b, wn)
+            m[f"uniform_1e8_s42/P{P}/max_rel_err"] = np.float64(np.max(np.abs(masses - w) / w))
+    print("uniform 1e8 done", flush=True)
+    np.savez_compressed(os.path.join(HERE, "psa_large.npz"), **m)
+
+
+def sweep_top(R):
+    """BASELINE configs[4]'s largest sizes that fit this host: n = 2^28
+    uniform and power-law s = 0.5 (seed 42) tables at the default job count,
+    appended to psa_large.npz (2^30 needs ~60 GB of host memory here)."""
+    path = os.path.join(HERE, "psa_large.npz")
+    m = dict(np.load(path))
+    n = 2**28
+    for tag, w in (("uniform_2p28_s42", lambda: R.generate_uniform(n, 42)),
+                   ("pl05_2p28_s42", lambda: R.generate_powerlaw(n, 0.5, 42))):
+        w = w()
+        m[f"{tag}/w_sha"] = sha(w)
+        P = default_jobs(n)
+        m[f"{tag}/jobs"] = np.array([P], np.uint64)
+        b, wn = R.psa_build_jobs(w, P, 8)
+        h = hashlib.sha256()
+        h.update(memoryview(b).cast("B"))
+        m[f"{tag}/P{P}/buckets_sha"] = h.hexdigest()
+        m[f"{tag}/P{P}/bucket_mean"] = np.float64(wn)
+        del b, w
+        print(tag, "done", flush=True)
+    np.savez_compressed(path, **m)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["two_level"]:
+    if sys.argv[1:] == ["large"]:
+        large(oracle.ref())
+        sweep_top(oracle.ref())
+    elif sys.argv[1:] == ["sweep_top"]:
+        sweep_top(oracle.ref())
+    elif sys.argv[1:] == ["two_level"]:
         two_level(oracle.ref())
     elif sys.argv[1:] == ["medium"]:
         medium(oracle.ref())

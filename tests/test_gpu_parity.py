@@ -449,3 +449,30 @@ def test_region_plan_larger_tiles_bit_exact(P, tt, monkeypatch):
         items, counts = S.draw_counts(31, k, Wk)
         ri, rc = np.unique(P.sample_many(b, S.bucket_mean, 31, k, Wk), return_counts=True)
         assert np.array_equal(items, ri) and np.array_equal(counts, rc)
+
+
+@pytest.mark.parametrize("ov_cap", [2_000_000, 4096])
+def test_region_plan_slab_redirect_and_overflow(P, ov_cap, monkeypatch):
+    """Slabs shrunk below the draws they receive (WRS_B200_TEST_SLAB_CAP):
+    runs that do not fit go to the overflow slab (ov_cap large: the gather
+    must stop at the first run that did not fit, never reading the unwritten
+    tail of the slab) or overflow it too (ov_cap tiny: the unpermute recomputes
+    the chunk directly).  Draws and counts stay bit-exact either way."""
+    import torch
+    monkeypatch.setenv("WRS_B200_PLAN", "r")
+    monkeypatch.setenv("WRS_B200_REGION_SHIFT", "16")   # 16 regions of 2^16 buckets
+    monkeypatch.setenv("WRS_B200_TEST_SLAB_CAP", "100000")
+    monkeypatch.setenv("WRS_B200_TEST_OV_CAP", str(ov_cap))
+    n, k = 1_000_003, 2_000_011  # ~125k draws per region: a fifth of every slab redirected
+    w = P.generate_powerlaw(n, 0.5, 3)
+    W, S = build(w)
+    b = S.buckets()
+    for Wk in (1, 5):
+        ref = P.sample_many(b, S.bucket_mean, 31, k, Wk)
+        out = torch.empty(k, dtype=torch.int32, device="cuda")
+        S.draw_device(31, k, Wk, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref), Wk
+        items, counts = S.draw_counts(31, k, Wk)
+        ri, rc = np.unique(ref, return_counts=True)
+        assert np.array_equal(items, ri) and np.array_equal(counts, rc), Wk
