@@ -116,8 +116,9 @@ WRS_API wrs_status wrs_b200_sampler_implied_masses(const wrs_sampler* s, double*
  * "counts" (u64 nl, nh), "heavy" (u32 heavy ids), "light_w", "heavy_w" (f64),
  * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries), "block_totals",
  * "carries" (f64, light blocks then heavy blocks), "split_light",
- * "split_heavy" (u32, P + 1), "split_spill" (f64, P + 1), "light_alias"
- * (u32, nl), "heavy_share" (f64, nh), "heavy_alias" (u32, nh).  *bytes
+ * "split_heavy" (u32, P + 1), "split_spill" (f64, P + 1), "light_rank"
+ * (u32, nl: the heavy rank j each light was paired with; its alias is
+ * heavy[min(j, nh-1)]), "heavy_share" (f64, nh).  *bytes
  * receives the size; host_out may be NULL to query it. */
 WRS_API wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name,
                                           void* host_out, uint64_t capacity,

@@ -1070,15 +1070,12 @@ wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name, void* 
         if (nm == "counts") {
             src = counts;
             by = sizeof counts;
-        } else if (nm == "light_alias") {
-            src = s->ws.lalias;
+        } else if (nm == "light_rank") {
+            src = s->ws.lrank;
             by = nl * 4;
         } else if (nm == "heavy_share") {
             src = s->ws.hshare;
             by = nh * 8;
-        } else if (nm == "heavy_alias") {
-            src = s->ws.halias;
-            by = nh * 4;
         } else if (nm == "heavy") {
             src = s->ws.hidx;
             by = nh * 4;

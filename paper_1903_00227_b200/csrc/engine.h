@@ -48,10 +48,9 @@ struct Workspace {
     double* hw = nullptr;            // gathered heavy weights
     double* lpre = nullptr;          // exclusive light prefix, nl + 1 entries
     double* hpre = nullptr;          // exclusive heavy prefix, nh + 1 entries
-    uint32_t* lalias = nullptr;      // K4a: alias of every light, list order
+    uint32_t* lrank = nullptr;       // K4a: alias heavy RANK of every light, list order
     double* hshare = nullptr;        // K4a: share of every heavy, list order
-    uint32_t* halias = nullptr;      // K4a: alias of every heavy, list order
-    uint32_t* lalias_own = nullptr;  // separate storage (else lalias aliases lpre)
+    uint32_t* lrank_own = nullptr;   // separate storage (else lrank aliases lpre)
     double* hshare_own = nullptr;    // separate storage (else hshare aliases hpre)
     double* totals = nullptr;        // K2a block totals (light blocks, then heavy)
     double* carries = nullptr;       // K2b exclusive carries

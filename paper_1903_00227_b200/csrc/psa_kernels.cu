@@ -987,72 +987,150 @@ k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__
 
 // ===========================================================================
 // K4a: pack (psa_pack, alias.hpp:160-209) -- one lane per job
-//   Each lane runs its job's sequential compensated sweep.  Work proceeds in
-//   phases of K4_S steps; before a phase the warp stages, for every lane, the
-//   next K4_S light weights and K4_S+1 heavy (weight, id) pairs with
-//   coalesced async copies, and after it flushes what the lanes produced in
-//   LIST order: the alias of every light and the (share, alias) of every
-//   heavy.  K4b turns those into index-ordered 16-B buckets with full-line
-//   stores (scattered 16-B bucket stores here would be half-sector writes,
-//   which the ECC-protected HBM turns into read-modify-writes).
+//   Each lane runs its job's sequential compensated sweep (the remainder
+//   chain is not associative, so a job IS a sequential chain; parallelism is
+//   the job count).  The lane's light and heavy weights stream through two
+//   per-lane rings of K4_R doubles in shared memory, refilled one phase
+//   ahead by warp-wide coalesced async copies (one half-warp per lane's row),
+//   so the copies of phase p+1 are in flight while phase p sweeps.  Outputs
+//   are written back in place (a light slot's low word takes its alias rank,
+//   a heavy slot its share) and flushed per phase in list order:
+//     lrank[p]  = the heavy RANK j the light at list position p was paired
+//                 with (its alias is heavy[min(j, nh-1)], alias.hpp:186-197),
+//     hshare[j] = the share of the heavy at list position j.
+//   The heavy ids are never read here: K4b maps ranks to ids, and a heavy's
+//   alias is always heavy[min(j+1, nh-1)] (alias.hpp:175-183, 200-206), so it
+//   needs no output at all.
 // ===========================================================================
-// S = 30 and 11 warps per CTA: 644 B of windows per lane, so one CTA of 11
-// warps fills an SM's shared memory (226.7 KB).  At n = 1e8 (97657 jobs =
-// 3052 warps) the 1628 resident warps run the pack in 2 rounds; 32-step
-// phases (672 B per lane) allowed only 10 warps per SM, i.e. 3 rounds, the
-// last one with 6% of the warps.
-// measured at n = 1e8: S = 30 / 11 warps 0.98 ms (two rounds of 1628 warps),
-// S = 20 / 15 warps 1.51 ms, S = 14 / 21 warps (one round) 2.04 ms: the
-// per-phase staging and flush outweigh the extra warps
-#ifndef K4_S_DEF
-#define K4_S_DEF 30
-#endif
+constexpr int K4_S = 14;          // steps per phase (items consumed per list <= S)
+constexpr int K4_R = 32;          // ring slots per list (power of two, >= 2S + 4)
+constexpr int K4_RS = K4_R + 2;   // row stride in doubles (16-B aligned rows for the pair copies)
 #ifndef K4_WARPS_DEF
-#define K4_WARPS_DEF 11
+#define K4_WARPS_DEF 12           // 17.6 KB of rings per warp: 12 warps fill 211 KB
 #endif
-#ifndef K4_ROW_UNROLL
-#define K4_ROW_UNROLL 32  // full: 0.96 vs 0.98 ms at unroll 8
-#endif
-constexpr int K4_ROW_U = K4_ROW_UNROLL;
-#ifndef K4_STEP_UNROLL
-#define K4_STEP_UNROLL 1  // measured 0.945 ms vs 0.959 at 2, 0.963 at 4
-#endif
-constexpr int K4_STEP_U = K4_STEP_UNROLL;  // steps per unrolled step of the sweep loops  // rows per unrolled step of the staging / flush loops
-constexpr int K4_S = K4_S_DEF;          // steps per phase (= max items consumed per list)
-constexpr int K4_WARPS = K4_WARPS_DEF;  // warps per CTA (windows fill an SM's shared memory)
-constexpr int K4_LW = K4_S + 1;     // light window row stride (odd -> no bank conflicts)
-constexpr int K4_HWIN = K4_S + 2;   // heavy window entries (S + 1 lookahead)
-constexpr int K4_HW = K4_S + 3;     // heavy window row stride (odd -> no bank conflicts)
+constexpr int K4_WARPS = K4_WARPS_DEF;
+static_assert(2 * K4_S + 4 <= K4_R, "a refill must not reach the slots of unflushed outputs");
 
 enum : int { ST_MAIN = 0, ST_TAILA = 1, ST_TAILB = 2, ST_DONE = 3 };
 
-struct K4Smem {
-    double lw[32][K4_LW];     // light weight in, light alias (low word) out
-    double hw[32][K4_HW];     // heavy weight in, heavy share out
-    uint32_t hix[32][K4_HW];  // heavy id in, heavy alias out
-    uint4 desc[32];           // per-lane window / flush descriptor, read back as broadcasts
+struct __align__(16) K4Rings {
+    double l[32][K4_RS];  // light weights in, alias ranks (low word) out
+    double h[32][K4_RS];  // heavy weights in, shares out
+    uint4 pos[32];        // per lane: flush-light, flush-heavy, refill-light, refill-heavy starts
+    uint32_t cnt[32];     // per lane: the four counts, one byte each
 };
-static_assert(K4_WARPS * sizeof(K4Smem) <= 232448, "K4a windows exceed 227 KB of shared memory");
+static_assert(K4_WARPS * sizeof(K4Rings) <= 232448, "K4a rings exceed 227 KB of shared memory");
 
 __device__ __forceinline__ uint32_t& low_word(double& d) { return reinterpret_cast<uint32_t*>(&d)[0]; }
 
+// 16-B cp.async, ordered (compiler) after the preceding shared-memory reads of
+// this thread; the hardware issues it after them.
+__device__ __forceinline__ void cp_async16_ordered(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// The warp's per-phase data movement over its 32 rings.  Iteration t serves
+// rows 4t .. 4t+3, one quarter-warp each; lane q of a quarter handles the
+// aligned position pair (2q, 2q+1) past the even position at or below the
+// range start (plus 16 per extra pass), for all four ranges of its row:
+//   flush : lights [fi, fi + fl) -> lrank (ranks, low words of the light
+//           slots), heavies [fj, fj + fh) -> hshare (shares);
+//   refill: lights [lf, lf + rl) and heavies [hf, hf + rh), global -> ring,
+//           asynchronously, as 16-B pairs (an edge pair also rewrites the
+//           neighbouring slot: with its own input if that position is still
+//           ahead, or with the pair's other input into the slot of a position
+//           32 back, whose output this same pass has already read).
+// A refill may target a slot a flush of the same row reads in the same
+// iteration: the flush's loads feed its stores, which issue before the copy.
+template <int PASSES>
+__device__ __forceinline__ void k4_rows(K4Rings& R, const double* __restrict__ lw,
+                                        const double* __restrict__ hw, uint32_t* __restrict__ lrank,
+                                        double* __restrict__ hshare) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t q2 = 2u * (lane & 7);
+    const int quarter = lane >> 3;
+#pragma unroll 2
+    for (int t = 0; t < 8; ++t) {
+        const int r = 4 * t + quarter;
+        const uint4 d = R.pos[r];
+        const uint32_t c = R.cnt[r];
+        const uint32_t fle = d.x + (c & 0xffu), fhe = d.y + ((c >> 8) & 0xffu);
+        const uint32_t rle = d.z + ((c >> 16) & 0xffu), rhe = d.w + (c >> 24);
+        double* const Lr = R.l[r];
+        double* const Hr = R.h[r];
+#pragma unroll
+        for (int ps = 0; ps < PASSES; ++ps) {
+            const uint32_t off = q2 + 16u * ps;
+            // flush
+            {
+                const uint32_t b = (d.x & ~1u) + off;
+                const bool v0 = b >= d.x && b < fle, v1 = b + 1 < fle;
+                if (v0 || v1) {
+                    const uint32_t s = b & (K4_R - 1);
+                    const uint32_t r0 = low_word(Lr[s]), r1 = low_word(Lr[s + 1]);
+                    if (v0 && v1)
+                        *reinterpret_cast<uint2*>(lrank + b) = make_uint2(r0, r1);
+                    else if (v0)
+                        lrank[b] = r0;
+                    else
+                        lrank[b + 1] = r1;
+                }
+            }
+            {
+                const uint32_t b = (d.y & ~1u) + off;
+                const bool v0 = b >= d.y && b < fhe, v1 = b + 1 < fhe;
+                if (v0 || v1) {
+                    const uint32_t s = b & (K4_R - 1);
+                    const double s0 = Hr[s], s1 = Hr[s + 1];
+                    if (v0 && v1)
+                        *reinterpret_cast<double2*>(hshare + b) = make_double2(s0, s1);
+                    else if (v0)
+                        hshare[b] = s0;
+                    else
+                        hshare[b + 1] = s1;
+                }
+            }
+            // refill (pairs; the inputs have >= 64 B of slack past their ends)
+            {
+                const uint32_t b = (d.z & ~1u) + off;
+                if (b < rle && d.z < rle)
+                    cp_async16_ordered(&Lr[b & (K4_R - 1)], lw + b);
+            }
+            {
+                const uint32_t b = (d.w & ~1u) + off;
+                if (b < rhe && d.w < rhe)
+                    cp_async16_ordered(&Hr[b & (K4_R - 1)], hw + b);
+            }
+        }
+    }
+}
+
+// FIN: the weights' total is far below DBL_MAX, so the remainder and every
+// term stay finite and the comp_sum finite-check never fires (the fast
+// phases skip it).
+template <bool FIN>
 __global__ void __launch_bounds__(K4_WARPS * 32)
-k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
-       const uint32_t* __restrict__ hidx, const double* __restrict__ hw,
+k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* __restrict__ hw,
        const uint32_t* __restrict__ split_l, const uint32_t* __restrict__ split_h,
-       const double* __restrict__ split_s, uint32_t* __restrict__ lalias,
-       double* __restrict__ hshare, uint32_t* __restrict__ halias) {
+       const double* __restrict__ split_s, uint32_t* __restrict__ lrank,
+       double* __restrict__ hshare) {
     extern __shared__ __align__(16) unsigned char k4_smem[];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    K4Smem& S = reinterpret_cast<K4Smem*>(k4_smem)[wq];
-    const uint64_t nh = sc->nh;
-    if (nh == 0) return;  // all items tie with the mean: K4b fills (alias.hpp:288-297)
+    K4Rings& R = reinterpret_cast<K4Rings*>(k4_smem)[wq];
+    const uint64_t nh64 = sc->nh;
+    if (nh64 == 0) return;  // all items tie with the mean: K4b fills (alias.hpp:288-297)
+    const uint32_t hlast = static_cast<uint32_t>(nh64 - 1);  // last heavy position
     const double wn = sc->wn;
+    double* const Lr = R.l[lane];
+    double* const Hr = R.h[lane];
+    auto lslot = [&](uint32_t p) -> double& { return Lr[p & (K4_R - 1)]; };
+    auto hslot = [&](uint32_t p) -> double& { return Hr[p & (K4_R - 1)]; };
 
     const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + wq) * 32 + lane;
-    uint64_t i = 0, lhi = 0, j = 0, hhi = 0;
-    int state = ST_DONE;
-    CompSum rem{0.0, 0.0};
+    uint32_t i = 0, lhi = 0, j = 0, hhi = 0;
+    int mode = ST_DONE;
+    double rhi = 0.0, rlo = 0.0;  // the remainder, comp_sum (parallel.hpp:70-81)
     if (k < P) {
         i = split_l[k];
         lhi = split_l[k + 1];
@@ -1060,235 +1138,205 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw,
         hhi = split_h[k + 1];
         if (lhi < i || hhi < j) {
             atomicOr(&sc->plan_error, 1u);  // alias.hpp:230-231
+            lhi = i;
+            hhi = j;
         } else {
-            state = ST_MAIN;
-            rem.hi = j < nh ? split_s[k] : CUDART_INF;  // alias.hpp:168
+            mode = ST_MAIN;
+            rhi = j < nh64 ? split_s[k] : CUDART_INF;  // alias.hpp:168
         }
     }
+    // heavy weights the job reads: positions j+1 .. min(hhi, nh-1)
+    const uint32_t hlim = umin64(hhi, hlast);
+    const uint32_t hend = mode == ST_DONE ? 0u : hlim + 1;  // exclusive
+    uint32_t lfill = i, hfill = j + 1;  // next positions to fetch
+    uint32_t fi = i, fj = j;            // first positions not yet flushed
 
-    while (__any_sync(0xffffffffu, state != ST_DONE)) {
-        // ---- stage this phase's windows ------------------------------------
-        // Every lane posts its window (light start, heavy start, counts) to
-        // shared memory; the warp then copies row r with one broadcast read of
-        // lane r's descriptor (item indices fit 32 bits: n < 2^32).  hcnt <=
-        // K4_S + 2 = 32, so one copy per lane covers a heavy row.
-        const bool live = state != ST_DONE;
-        const uint64_t wl0 = i;
-        const int lcnt = live ? static_cast<int>(umin64(K4_S, lhi - i)) : 0;
-        const uint64_t wh0 = umin64(j, nh - 1);
-        const uint64_t hend = umin64(umin64(j + K4_S + 1, hhi + 1), nh);
-        const int hcnt = live ? static_cast<int>(hend - wh0) : 0;
-        S.desc[lane] = make_uint4(static_cast<uint32_t>(wl0), static_cast<uint32_t>(wh0),
-                                  static_cast<uint32_t>(lcnt | (hcnt << 8)), 0u);
+    // post this lane's flush [fi, i), [fj, j) and refill [lfill, i + 2S), [hfill, j + 1 + 2S)
+    // (refill ends are rounded up to even positions, so every refill after the
+    // prologue starts on a pair boundary and never rewrites a slot behind it;
+    // the one extra input read past a range end is never used)
+    auto post = [&]() {
+        const uint32_t lto = lhi - i > 2 * K4_S ? i + 2 * K4_S : lhi;
+        const uint32_t hto = (hend > j + 1 && hend - (j + 1) > 2 * K4_S) ? j + 1 + 2 * K4_S : hend;
+        const uint32_t rl = lto > lfill ? ((lto - lfill + (lfill & 1u) + 1u) & ~1u) - (lfill & 1u) : 0u;
+        const uint32_t rh = hto > hfill ? ((hto - hfill + (hfill & 1u) + 1u) & ~1u) - (hfill & 1u) : 0u;
+        R.pos[lane] = make_uint4(fi, fj, lfill, hfill);
+        R.cnt[lane] = (i - fi) | ((j - fj) << 8) | (rl << 16) | (rh << 24);
+        lfill += rl;
+        hfill += rh;
+        fi = i;
+        fj = j;
         __syncwarp();
-#pragma unroll K4_ROW_U
-        for (int r = 0; r < 32; ++r) {
-            const uint4 d = S.desc[r];
-            const int rlc = static_cast<int>(d.z & 0xffu), rhc = static_cast<int>(d.z >> 8);
-            if (lane < rlc) cp_async8(&S.lw[r][lane], lw + (d.x + lane));
-            if (lane < rhc) {
-                cp_async8(&S.hw[r][lane], hw + (d.y + lane));
-                cp_async4(&S.hix[r][lane], hidx + (d.y + lane));
+    };
+    post();
+    k4_rows<2>(R, lw, hw, lrank, hshare);  // prologue: two phases' worth of inputs
+    cp_async_commit();
+    cp_async_commit();  // (empty: phase 0 waits for the prologue alone)
+
+    while (__any_sync(0xffffffffu, mode != ST_DONE)) {
+        // this phase's inputs (posted two phases ago) have landed; the copies
+        // posted at the end of the last phase stay in flight
+        cp_async_wait<1>();
+        __syncwarp();
+        // Fast phase: every lane in the main loop with >= S lights and >= S
+        // next heavies left, so no tail loop or last-heavy reset can start:
+        // the step is the main loop's body alone (alias.hpp:175-189).
+        const bool fast = __all_sync(0xffffffffu, mode == ST_MAIN && lhi - i >= K4_S &&
+                                                      hlim >= j + K4_S);
+        if (fast) {
+#pragma unroll
+            for (int s = 0; s < K4_S; ++s) {
+                const double v = rhi + rlo;  // rem.value()
+                const bool gt = v > wn;
+                // the next light w[i] or the next heavy w[j+1], read once the
+                // direction is known
+                const double x = (gt ? lslot(i) : hslot(j + 1)) - wn;
+                // rem.add(x): the guarded Neumaier add, branch-free
+                const double t = rhi + x;
+                const bool big = fabs(rhi) >= fabs(x);
+                const double a = big ? rhi : x, b = big ? x : rhi;
+                const double l2 = rlo + ((a - t) + b);
+                rlo = (FIN || isfinite(t)) ? l2 : rlo;
+                rhi = t;
+                if (gt) {  // light bucket {w, {idx, heavy_at(j)}}: rank j
+                    low_word(lslot(i)) = j;
+                } else {   // heavy bucket {max(0, min(rem, wn)), ...}; rem <= wn here,
+                           // so the share is rem if rem > 0 else +0.0
+                    const long long vb = __double_as_longlong(v);
+                    hslot(j) = __longlong_as_double(v > 0.0 ? vb : 0ll);
+                }
+                i += gt;
+                j += !gt;
+            }
+        } else {
+#pragma unroll 2
+            for (int s = 0; s < K4_S; ++s) {
+                const double v = rhi + rlo;
+                const bool gt = v > wn;
+                const bool lightsLeft = i < lhi, heaviesLeft = j < hhi;
+                int st = mode;
+                if (st == ST_MAIN && gt && !lightsLeft) st = ST_TAILA;   // alias.hpp:172
+                if (st == ST_MAIN && !gt && !heaviesLeft) st = ST_TAILB; // alias.hpp:191
+                const bool isMain = st == ST_MAIN;
+                const bool lightOp = (isMain && gt) || (st == ST_TAILB && lightsLeft);
+                const bool heavyOp = (isMain && !gt) || (st == ST_TAILA && heaviesLeft);
+                if (!lightOp && !heavyOp) st = ST_DONE;  // tail loops exhausted: return
+                mode = st;
+                // remainder: rem.add(w - wn), or the reset at the last heavy
+                const bool hasNext = j < hlast;
+                const double x = (lightOp ? lslot(i) : hslot(j + 1)) - wn;
+                const bool doAdd = (lightOp && isMain) || (heavyOp && hasNext);
+                const bool doReset = heavyOp && !hasNext;
+                const double t = rhi + x;
+                const bool big = fabs(rhi) >= fabs(x);
+                const double a = big ? rhi : x, b = big ? x : rhi;
+                const double l2 = rlo + ((a - t) + b);
+                const double nlo = isfinite(t) ? l2 : rlo;
+                const double resetHi = isMain ? CUDART_INF : wn;  // rem = {inf} / rem = {wn}
+                // light bucket {w, {idx, heavy_at(j)}} (alias.hpp:186-189, 194-197)
+                if (lightOp) low_word(lslot(i)) = j;
+                // heavy bucket {clamp(rem), {idx, heavy_at(j+1)}} (alias.hpp:175-183, 200-206)
+                if (heavyOp) hslot(j) = isMain ? std_max(0.0, std_min(v, wn)) : std_min(v, wn);
+                rhi = doAdd ? t : (doReset ? resetHi : rhi);
+                rlo = doAdd ? nlo : (doReset ? 0.0 : rlo);
+                i += lightOp;
+                j += heavyOp;
             }
         }
+        __syncwarp();
+        // this phase's outputs out, the phase after next's inputs in
+        post();
+        k4_rows<1>(R, lw, hw, lrank, hshare);
         cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
-
-        // Prefetch into L2 the lines the next phase's windows most likely
-        // need ([i+S, i+2S) and the heavy run after this window), so the next
-        // staging copies hit L2 instead of HBM.
-        if (live) {
-            const char* pl = reinterpret_cast<const char*>(lw + umin64(wl0 + K4_S, lhi));
-            const char* ph = reinterpret_cast<const char*>(hw + umin64(wh0 + K4_S, nh - 1));
-            const char* pi = reinterpret_cast<const char*>(hidx + umin64(wh0 + K4_S, nh - 1));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pl));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pl + 128));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ph));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ph + 128));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pi));
-        }
-
-        // ---- up to K4_S sequential steps per lane ---------------------------
-        // Branch-free: every lane evaluates the same instruction stream, the
-        // operation (light bucket / heavy bucket / none) is a predicate.
-        // Window-relative 32-bit cursors: li = i - wl0, hj = j - wh0.
-        const uint64_t i0 = i, j0 = j;
-        const int lrem = live ? static_cast<int>(umin64(lhi - i, K4_S + 1)) : 0;  // i < lhi
-        const int hrem = live ? static_cast<int>(umin64(hhi - wh0, K4_S + 2)) : 0; // j < hhi
-        const int hlast = static_cast<int>(umin64(nh - 1 - wh0, K4_S + 2));        // j+1 < nh
-        int li = 0, hj = static_cast<int>(j - wh0);
-        double cLw = S.lw[lane][0];
-        uint32_t hCur = S.hix[lane][0];  // heavy_at(j): slot of min(j, nh-1) = wh0
-        int qn = min(min(hj + 1, hlast), K4_HWIN - 1);
-        uint32_t hNext = S.hix[lane][qn];
-        double hNextW = S.hw[lane][qn];
-        // Fast phase: every lane of the warp is in the main loop with more
-        // than K4_S lights and K4_S + 1 heavies (and a next heavy) left, so no
-        // tail loop or last-heavy reset can start within this phase: the step
-        // is the main loop's body alone (alias.hpp:175-189), identical values.
-        const bool fast = __all_sync(0xffffffffu, state == ST_MAIN && lrem == K4_S + 1 &&
-                                                      hrem == K4_S + 2 && hlast == K4_S + 2);
-#pragma unroll K4_STEP_U
-        for (int step = 0; fast && step < K4_S; ++step) {
-            const double v = rem.value();
-            const bool gt = v > wn;
-            rem.add((gt ? cLw : hNextW) - wn);
-            if (gt) {  // light bucket {w, {idx, heavy_at(j)}}
-                low_word(S.lw[lane][li]) = hCur;
-                ++li;
-                cLw = S.lw[lane][min(li, K4_S - 1)];
-            } else {   // heavy bucket {clamp(rem), {idx, heavy_at(j+1)}}
-                S.hw[lane][hj] = std_max(0.0, std_min(v, wn));
-                S.hix[lane][hj] = hNext;
-                ++hj;
-                hCur = hNext;
-                hNext = S.hix[lane][hj + 1];
-                hNextW = S.hw[lane][hj + 1];
-            }
-        }
-#pragma unroll K4_STEP_U
-        for (int step = 0; !fast && step < K4_S; ++step) {
-            const double v = rem.value();
-            const bool gt = v > wn;
-            const bool lightsLeft = li < lrem, heaviesLeft = hj < hrem;
-            int st = state;
-            if (st == ST_MAIN && gt && !lightsLeft) st = ST_TAILA;   // alias.hpp:172
-            if (st == ST_MAIN && !gt && !heaviesLeft) st = ST_TAILB; // alias.hpp:191
-            const bool isMain = st == ST_MAIN;
-            const bool lightOp = (isMain && gt) || (st == ST_TAILB && lightsLeft);
-            const bool heavyOp = (isMain && !gt) || (st == ST_TAILA && heaviesLeft);
-            if (!lightOp && !heavyOp) st = ST_DONE;  // tail loops exhausted: return
-            state = st;
-            // remainder update: rem.add(w - wn), or the reset at the last heavy
-            const bool hasNext = hj < hlast;
-            const double d = (lightOp ? cLw : hNextW) - wn;
-            const bool doAdd = (lightOp && isMain) || (heavyOp && hasNext);
-            const bool doReset = heavyOp && !hasNext;
-            CompSum nr = rem;
-            nr.add(d);
-            const double resetHi = isMain ? CUDART_INF : wn;  // rem = {inf} / rem = {wn}
-            rem.hi = doAdd ? nr.hi : (doReset ? resetHi : rem.hi);
-            rem.lo = doAdd ? nr.lo : (doReset ? 0.0 : rem.lo);
-            // light bucket {w, {idx, heavy_at(j)}} (alias.hpp:186-189, 194-197)
-            if (lightOp) low_word(S.lw[lane][li]) = hCur;
-            // heavy bucket {clamp(rem), {idx, heavy_at(j+1)}} (alias.hpp:175-183, 200-206)
-            if (heavyOp) {
-                S.hw[lane][hj] = isMain ? std_max(0.0, std_min(v, wn)) : std_min(v, wn);
-                S.hix[lane][hj] = hNext;
-            }
-            li += lightOp;
-            hj += heavyOp;
-            if (lightOp) cLw = S.lw[lane][min(li, K4_S - 1)];
-            if (heavyOp) {
-                hCur = hNext;
-                qn = min(min(hj + 1, hlast), K4_HWIN - 1);
-                hNext = S.hix[lane][qn];
-                hNextW = S.hw[lane][qn];
-            }
-        }
-        i = wl0 + li;
-        j = wh0 + hj;
-        __syncwarp();
-
-        // ---- flush this phase's outputs in list order ----------------------
-        const int nlw = static_cast<int>(i - i0);
-        const int nhw = static_cast<int>(j - j0);
-        const int hoff = static_cast<int>(j0 - wh0);
-        S.desc[lane] = make_uint4(static_cast<uint32_t>(i0), static_cast<uint32_t>(j0),
-                                  static_cast<uint32_t>(nlw | (nhw << 8) | (hoff << 16)), 0u);
-        __syncwarp();
-#pragma unroll K4_ROW_U
-        for (int r = 0; r < 32; ++r) {
-            const uint4 d = S.desc[r];
-            const int rl = static_cast<int>(d.z & 0xffu), rh = static_cast<int>((d.z >> 8) & 0xffu);
-            const int ro = static_cast<int>(d.z >> 16);
-            if (lane < rl) lalias[d.x + lane] = low_word(S.lw[r][lane]);
-            if (lane < rh) {
-                hshare[d.y + lane] = S.hw[r][ro + lane];
-                halias[d.y + lane] = S.hix[r][ro + lane];
-            }
-        }
-        __syncwarp();
     }
+    cp_async_wait<0>();
 }
 
 // ===========================================================================
 // K4b: assemble the 16-B buckets in index order (one CTA per K1 tile)
-//   light item i : {w_i, i, lalias[light rank]}      (alias.hpp:186-197)
-//   heavy item i : {hshare[rank], i, halias[rank]}   (alias.hpp:175-206)
-//   no heavy at all: {w_i, i, i}                     (alias.hpp:288-297)
+//   light item i : {w_i, i, heavy[min(lrank[rank of i], nh-1)]}  (alias.hpp:186-197)
+//   heavy item i : {hshare[rank], i, heavy[min(rank+1, nh-1)]}    (alias.hpp:175-206)
+//   no heavy at all: {w_i, i, i}                                  (alias.hpp:288-297)
 //   Ranks come from the same tile classification as K1 plus K1's inclusive
 //   tile prefix; every warp stores 32 consecutive buckets = 512 contiguous B.
 // ===========================================================================
 #ifndef K4B_SMEM_KB
-#define K4B_SMEM_KB 40
+#define K4B_SMEM_KB 32
 #endif
-constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // staging budget: 5 CTAs per SM at 40 KB
+constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // the tile's lrank + hshare runs always fit
 #ifndef K4B_ROW_UNROLL
 #define K4B_ROW_UNROLL 4
 #endif
 constexpr int K4B_ROW_U = K4B_ROW_UNROLL;
 __global__ void __launch_bounds__(K1_THREADS)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
-           const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lalias,
-           const double* __restrict__ hshare, const uint32_t* __restrict__ halias,
+           const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lrank,
+           const double* __restrict__ hshare, const uint32_t* __restrict__ hidx,
            Bucket* __restrict__ out) {
     // The tile's lights are the contiguous light-list run [L0, L0 + totL) and
     // its heavies the run [H0, H0 + totH): both runs are staged into shared
-    // memory with coalesced async copies, then every item reads its alias /
-    // share from there (measured: reading them straight from global memory,
-    // at 7 CTAs/SM instead of 4, is slower: 0.70 vs 0.65 ms at n = 1e8).
+    // memory with coalesced async copies (4 totL + 8 totH <= 32 KB).  The
+    // heavy ids the aliases need are read straight from `heavy`: a warp's 32
+    // items reference a short nondecreasing run of ranks (lights) or the run
+    // right after its own heavies, so those loads coalesce.
     extern __shared__ __align__(16) unsigned char k4b_smem[];
     __shared__ TileCells C;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t tile = blockIdx.x;
     const uint64_t base = tile * K1_TILE;
-    const bool uniform = sc->nh == 0;
+    const uint64_t nh = sc->nh;
     classify_tile<false>(w, n, base, sc->wn, nullptr, C);
+    if (nh == 0) {  // fill_uniform_if_no_heavy (alias.hpp:288-297)
+#pragma unroll 4
+        for (int r = 0; r < K1_ROWS; ++r) {
+            const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
+            if (gi < n) store_bucket(out, gi, __ldg(w + gi), static_cast<uint32_t>(gi),
+                                     static_cast<uint32_t>(gi));
+        }
+        return;
+    }
     const uint32_t totL = C.totL, totH = C.totH;
     const uint64_t L0 = (status[tile] & VAL_MASK) - totL;
     const uint64_t H0 = base - L0;
-    // staged when the tile's runs fit the budget (every tile but nearly-all-
-    // heavy ones), else read straight from global memory
-    const bool staged = ((4u * totL + 15u) & ~15u) + 12u * totH <= K4B_SMEM;
-    const uint32_t* s_la = lalias + L0;
-    const double* s_hs = hshare + H0;
-    const uint32_t* s_ha = halias + H0;
-    if (!uniform && staged) {
-        uint32_t* d_la = reinterpret_cast<uint32_t*>(k4b_smem);
-        double* d_hs = reinterpret_cast<double*>(k4b_smem + ((4u * totL + 15u) & ~15u));
-        uint32_t* d_ha = reinterpret_cast<uint32_t*>(d_hs + totH);
-        s_la = d_la;
-        s_hs = d_hs;
-        s_ha = d_ha;
-        for (uint32_t i = threadIdx.x; i < totL; i += K1_THREADS) cp_async4(&d_la[i], lalias + L0 + i);
-        for (uint32_t i = threadIdx.x; i < totH; i += K1_THREADS) {
-            cp_async8(&d_hs[i], hshare + H0 + i);
-            cp_async4(&d_ha[i], halias + H0 + i);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-    }
+    const uint32_t b_la = (4u * totL + 15u) & ~15u;
+    uint32_t* d_la = reinterpret_cast<uint32_t*>(k4b_smem);
+    double* d_hs = reinterpret_cast<double*>(k4b_smem + b_la);
+    for (uint32_t q = threadIdx.x; q < totL; q += K1_THREADS) cp_async4(&d_la[q], lrank + L0 + q);
+    for (uint32_t q = threadIdx.x; q < totH; q += K1_THREADS) cp_async8(&d_hs[q], hshare + H0 + q);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     const unsigned lt = lanemask_lt();
-#pragma unroll K4B_ROW_U
-    for (int r = 0; r < K1_ROWS; ++r) {
-        const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
-        if (gi >= n) continue;
-        const int cell = r * K1_WARPS + warp;
-        const unsigned lm = C.lm[cell];
-        double share;
-        uint32_t alias = static_cast<uint32_t>(gi);
-        if ((lm >> lane) & 1) {
-            share = __ldg(w + gi);
-            if (!uniform) alias = s_la[C.exL[cell] + __popc(lm & lt)];
-        } else {
-            const uint32_t p = C.exH[cell] + __popc(C.hm[cell] & lt);
-            share = s_hs[p];
-            alias = s_ha[p];
+    const uint32_t hmax = static_cast<uint32_t>(nh - 1);
+    // half a tile at a time: all of its share / id loads in flight, then the
+    // stores
+    constexpr int HR = K1_ROWS / 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double xs[HR];
+        uint32_t ids[HR];
+#pragma unroll
+        for (int u = 0; u < HR; ++u) {
+            const int r = h * HR + u;
+            const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
+            const int cell = r * K1_WARPS + warp;
+            const unsigned lm = C.lm[cell];
+            uint32_t rank;
+            if ((lm >> lane) & 1) {
+                xs[u] = gi < n ? __ldg(w + gi) : 0.0;
+                rank = min(d_la[C.exL[cell] + __popc(lm & lt)], hmax);  // heavy_at(j)
+            } else {
+                const uint32_t q = C.exH[cell] + __popc(C.hm[cell] & lt);
+                xs[u] = d_hs[q];
+                rank = min(static_cast<uint32_t>(H0) + q + 1, hmax);  // heavy_at(j + 1)
+            }
+            ids[u] = gi < n ? __ldg(hidx + rank) : 0u;
         }
-        store_bucket(out, gi, share, static_cast<uint32_t>(gi), alias);
+#pragma unroll
+        for (int u = 0; u < HR; ++u) {
+            const uint64_t gi = base + (h * HR + u) * K1_THREADS + threadIdx.x;
+            if (gi < n) store_bucket(out, gi, xs[u], static_cast<uint32_t>(gi), ids[u]);
+        }
     }
 }
 
@@ -1330,7 +1378,6 @@ cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate
     A(ws.hw, n);
     A(ws.lpre, n + 1);
     A(ws.hpre, n + 1);
-    A(ws.halias, n);
     A(ws.totals, nblocks);
     A(ws.carries, nblocks);
     A(ws.split_l, P + 1);
@@ -1338,13 +1385,13 @@ cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate
     A(ws.split_s, P + 1);
     A(ws.sc, 1);
     if (separate_outputs) {
-        A(ws.lalias_own, n);
+        A(ws.lrank_own, n);
         A(ws.hshare_own, n);
-        ws.lalias = ws.lalias_own;
+        ws.lrank = ws.lrank_own;
         ws.hshare = ws.hshare_own;
     } else {
         // K4a runs after K3, the last reader of the prefix arrays: reuse them.
-        ws.lalias = reinterpret_cast<uint32_t*>(ws.lpre);
+        ws.lrank = reinterpret_cast<uint32_t*>(ws.lpre);
         ws.hshare = ws.hpre;
     }
     if (e != cudaSuccess) workspace_free(ws);
@@ -1364,9 +1411,9 @@ cudaError_t workspace_alloc_total(Workspace& ws, uint64_t n) {
 
 void workspace_free(Workspace& ws) {
     void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.hidx,       ws.lw,
-                    ws.hw,       ws.lpre,     ws.hpre,        ws.halias,     ws.totals,
+                    ws.hw,       ws.lpre,     ws.hpre,        ws.totals,
                     ws.carries,  ws.split_l,  ws.split_h,     ws.split_s,    ws.sc,
-                    ws.lalias_own, ws.hshare_own};
+                    ws.lrank_own, ws.hshare_own};
     for (void* p : ptrs)
         if (p) dev_free(p);
     ws = Workspace{};
@@ -1436,10 +1483,11 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     const uint64_t k4_warps_total = (P + 31) / 32;
     const int k4_warps = static_cast<int>(std::min<uint64_t>(
         K4_WARPS, std::max<uint64_t>(1, (k4_warps_total + 147) / 148)));
-    const int k4_smem = k4_warps * static_cast<int>(sizeof(K4Smem));
+    const int k4_smem = k4_warps * static_cast<int>(sizeof(K4Rings));
     // per-device attribute; cheap enough to set on every build
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem);
-    cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
+    cudaFuncSetAttribute(k_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
+    cudaFuncSetAttribute(k_pack<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
     cudaFuncSetAttribute(k_scan_carry_split, cudaFuncAttributeMaxDynamicSharedMemorySize, K2W_SMEM);
     cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, K4B_SMEM);
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
@@ -1500,12 +1548,15 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
                                      ws.split_s);
     REC(5);
-    k_pack<<<k4_grid, k4_warps * 32, k4_smem, st>>>(P, ws.sc, ws.lw, ws.hidx, ws.hw, ws.split_l,
-                                                    ws.split_h, ws.split_s, ws.lalias, ws.hshare,
-                                                    ws.halias);
+    if (pos)  // W < 1e300: the remainder stays finite
+        k_pack<true><<<k4_grid, k4_warps * 32, k4_smem, st>>>(
+            P, ws.sc, ws.lw, ws.hw, ws.split_l, ws.split_h, ws.split_s, ws.lrank, ws.hshare);
+    else
+        k_pack<false><<<k4_grid, k4_warps * 32, k4_smem, st>>>(
+            P, ws.sc, ws.lw, ws.hw, ws.split_l, ws.split_h, ws.split_s, ws.lrank, ws.hshare);
     REC(6);
     k_assemble<<<static_cast<unsigned>(ntiles), K1_THREADS, K4B_SMEM, st>>>(
-        d_w, n, ws.sc, ws.tile_status, ws.lalias, ws.hshare, ws.halias, d_b);
+        d_w, n, ws.sc, ws.tile_status, ws.lrank, ws.hshare, ws.hidx, d_b);
     REC(7);
 #undef REC
     return cudaGetLastError();

@@ -488,8 +488,10 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
 // cursor[0, nreg) are the region fill cursors, cursor[nreg] the overflow
 // slab's, cursor[nreg + 1 + r] the base of region r's first run that did not
 // fit (~0 if none; every run claimed below it was written).
+// p0: a position inside the slab (the overflow slab may be longer than cap).
 __device__ __forceinline__ uint64_t slab_valid_end(const RegionGeom& rg, const uint32_t* cursor,
-                                                   uint32_t slab) {
+                                                   uint64_t p0) {
+    const uint32_t slab = static_cast<uint32_t>(umin64(p0 / rg.cap, rg.nreg));
     const uint64_t slab0 = static_cast<uint64_t>(slab) * rg.cap;
     if (slab < rg.nreg)
         return slab0 + umin64(umin64(cursor[slab], rg.cap), cursor[rg.nreg + 1 + slab]);
@@ -507,8 +509,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
                 uint32_t* __restrict__ res) {
     if (*overflow) return;  // the overflow slab overflowed: RD recomputes the chunk directly
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
-    const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);  // nreg = overflow slab
-    const uint64_t valid_end = slab_valid_end(rg, cursor, slab);
+    const uint64_t valid_end = slab_valid_end(rg, cursor, p0);
     if (p0 >= valid_end) return;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
@@ -662,8 +663,7 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
                uint32_t* __restrict__ hits) {
     if (*overflow) return;  // k_count_direct<.., true> recounts the chunk
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
-    const uint32_t slab = static_cast<uint32_t>(p0 / rg.cap);
-    const uint64_t valid_end = slab_valid_end(rg, cursor, slab);
+    const uint64_t valid_end = slab_valid_end(rg, cursor, p0);
     if (p0 >= valid_end) return;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;

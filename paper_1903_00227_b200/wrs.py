@@ -346,8 +346,8 @@ class Sampler:
             _stream_ptr(stream, items)))
 
     def stage(self, name: str) -> np.ndarray:
-        dtypes = {"counts": np.uint64, "heavy": np.uint32, "light_alias": np.uint32,
-                  "heavy_share": np.float64, "heavy_alias": np.uint32,
+        dtypes = {"counts": np.uint64, "heavy": np.uint32, "light_rank": np.uint32,
+                  "heavy_share": np.float64,
                   "light_w": np.float64, "heavy_w": np.float64, "light_prefix": np.float64,
                   "heavy_prefix": np.float64, "block_totals": np.float64,
                   "carries": np.float64, "split_light": np.uint32, "split_heavy": np.uint32,

@@ -1,7 +1,9 @@
 """Per-kernel build times (CUDA events inside the library) for A/B builds:
     WRS_B200_LIB=... python scripts/stage_probe.py [n] [reps]"""
+import os
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: F401  (CUDA context)
 
 import paper_1903_00227_b200 as wrs
