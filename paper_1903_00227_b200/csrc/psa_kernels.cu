@@ -1261,24 +1261,25 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* 
 //   tile prefix; every warp stores 32 consecutive buckets = 512 contiguous B.
 // ===========================================================================
 #ifndef K4B_SMEM_KB
-#define K4B_SMEM_KB 32
+#define K4B_SMEM_KB 36
 #endif
-constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // the tile's lrank + hshare runs always fit
-#ifndef K4B_ROW_UNROLL
-#define K4B_ROW_UNROLL 4
-#endif
-constexpr int K4B_ROW_U = K4B_ROW_UNROLL;
+constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // 6 CTAs per SM
+constexpr uint32_t K4B_PAD = 64;  // heavy ids staged either side of the tile's own
 __global__ void __launch_bounds__(K1_THREADS)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
            const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lrank,
            const double* __restrict__ hshare, const uint32_t* __restrict__ hidx,
            Bucket* __restrict__ out) {
     // The tile's lights are the contiguous light-list run [L0, L0 + totL) and
-    // its heavies the run [H0, H0 + totH): both runs are staged into shared
-    // memory with coalesced async copies (4 totL + 8 totH <= 32 KB).  The
-    // heavy ids the aliases need are read straight from `heavy`: a warp's 32
-    // items reference a short nondecreasing run of ranks (lights) or the run
-    // right after its own heavies, so those loads coalesce.
+    // its heavies the run [H0, H0 + totH): their lrank / hshare runs are
+    // staged into shared memory with coalesced async copies.  The aliases are
+    // heavy ids by rank: a heavy's is rank H0 + q + 1; a light's is the rank
+    // the pack paired it with, which lies within a few dozen of the tile's own
+    // heavy ranks (jobs balance light and heavy weight at every split).  So
+    // the ids of ranks [H0 - PAD, H0 + totH + PAD) are staged too -- the
+    // tile's own heavies write theirs (no load), the two PAD-wide edges are
+    // copied from `heavy` -- and only a rank outside that window (rare, or a
+    // tile whose runs do not fit the budget) reads `heavy` from global memory.
     extern __shared__ __align__(16) unsigned char k4b_smem[];
     __shared__ TileCells C;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1286,6 +1287,7 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     const uint64_t base = tile * K1_TILE;
     const uint64_t nh = sc->nh;
     classify_tile<false>(w, n, base, sc->wn, nullptr, C);
+    const unsigned lt = lanemask_lt();
     if (nh == 0) {  // fill_uniform_if_no_heavy (alias.hpp:288-297)
 #pragma unroll 4
         for (int r = 0; r < K1_ROWS; ++r) {
@@ -1298,45 +1300,55 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     const uint32_t totL = C.totL, totH = C.totH;
     const uint64_t L0 = (status[tile] & VAL_MASK) - totL;
     const uint64_t H0 = base - L0;
+    const uint64_t wlo = H0 > K4B_PAD ? H0 - K4B_PAD : 0;
+    const uint64_t whi = umin64(H0 + totH + K4B_PAD, nh);
     const uint32_t b_la = (4u * totL + 15u) & ~15u;
+    const uint32_t b_hs = 8u * totH;
+    const bool ids = b_la + b_hs + 4u * static_cast<uint32_t>(whi - wlo) <= K4B_SMEM;
     uint32_t* d_la = reinterpret_cast<uint32_t*>(k4b_smem);
     double* d_hs = reinterpret_cast<double*>(k4b_smem + b_la);
+    uint32_t* d_id = reinterpret_cast<uint32_t*>(k4b_smem + b_la + b_hs);  // ranks [wlo, whi)
     for (uint32_t q = threadIdx.x; q < totL; q += K1_THREADS) cp_async4(&d_la[q], lrank + L0 + q);
     for (uint32_t q = threadIdx.x; q < totH; q += K1_THREADS) cp_async8(&d_hs[q], hshare + H0 + q);
+    if (ids) {
+        const uint32_t e0 = static_cast<uint32_t>(H0 - wlo), e1 = static_cast<uint32_t>(H0 + totH - wlo);
+        const uint32_t e2 = static_cast<uint32_t>(whi - wlo);
+        for (uint32_t q = threadIdx.x; q < e0; q += K1_THREADS) cp_async4(&d_id[q], hidx + wlo + q);
+        for (uint32_t q = e1 + threadIdx.x; q < e2; q += K1_THREADS) cp_async4(&d_id[q], hidx + wlo + q);
+        // the tile's own heavies: rank H0 + q is item gi
+#pragma unroll 4
+        for (int r = 0; r < K1_ROWS; ++r) {
+            const int cell = r * K1_WARPS + warp;
+            const unsigned hm = C.hm[cell];
+            if ((hm >> lane) & 1)
+                d_id[e0 + C.exH[cell] + __popc(hm & lt)] =
+                    static_cast<uint32_t>(base + r * K1_THREADS + threadIdx.x);
+        }
+    }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    const unsigned lt = lanemask_lt();
     const uint32_t hmax = static_cast<uint32_t>(nh - 1);
-    // half a tile at a time: all of its share / id loads in flight, then the
-    // stores
-    constexpr int HR = K1_ROWS / 2;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        double xs[HR];
-        uint32_t ids[HR];
-#pragma unroll
-        for (int u = 0; u < HR; ++u) {
-            const int r = h * HR + u;
-            const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
-            const int cell = r * K1_WARPS + warp;
-            const unsigned lm = C.lm[cell];
-            uint32_t rank;
-            if ((lm >> lane) & 1) {
-                xs[u] = gi < n ? __ldg(w + gi) : 0.0;
-                rank = min(d_la[C.exL[cell] + __popc(lm & lt)], hmax);  // heavy_at(j)
-            } else {
-                const uint32_t q = C.exH[cell] + __popc(C.hm[cell] & lt);
-                xs[u] = d_hs[q];
-                rank = min(static_cast<uint32_t>(H0) + q + 1, hmax);  // heavy_at(j + 1)
-            }
-            ids[u] = gi < n ? __ldg(hidx + rank) : 0u;
+    const uint32_t wlo32 = static_cast<uint32_t>(wlo), wn32 = static_cast<uint32_t>(whi - wlo);
+#pragma unroll 4
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
+        if (gi >= n) continue;
+        const int cell = r * K1_WARPS + warp;
+        const unsigned lm = C.lm[cell];
+        double share;
+        uint32_t rank;
+        if ((lm >> lane) & 1) {
+            share = __ldg(w + gi);
+            rank = min(d_la[C.exL[cell] + __popc(lm & lt)], hmax);  // heavy_at(j)
+        } else {
+            const uint32_t q = C.exH[cell] + __popc(C.hm[cell] & lt);
+            share = d_hs[q];
+            rank = min(static_cast<uint32_t>(H0) + q + 1, hmax);  // heavy_at(j + 1)
         }
-#pragma unroll
-        for (int u = 0; u < HR; ++u) {
-            const uint64_t gi = base + (h * HR + u) * K1_THREADS + threadIdx.x;
-            if (gi < n) store_bucket(out, gi, xs[u], static_cast<uint32_t>(gi), ids[u]);
-        }
+        const uint32_t o = rank - wlo32;
+        const uint32_t id = (ids && o < wn32) ? d_id[o] : __ldg(hidx + rank);
+        store_bucket(out, gi, share, static_cast<uint32_t>(gi), id);
     }
 }
 
