@@ -114,7 +114,9 @@ WRS_API wrs_status wrs_b200_sampler_implied_masses(const wrs_sampler* s, double*
 
 /* Copy a named intermediate of the last build (needs WRS_B200_KEEP_WORKSPACE):
  * "counts" (u64 nl, nh), "heavy" (u32 heavy ids), "light_w", "heavy_w" (f64),
- * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries), "block_totals",
+ * "light_prefix", "heavy_prefix" (f64, n_x + 1 entries; builds of large
+ * tables keep instead "light_ckpt", "heavy_ckpt": f64 (hi, lo) pairs, the
+ * prefix chain's state before every 16th element), "block_totals",
  * "carries" (f64, light blocks then heavy blocks), "split_light",
  * "split_heavy" (u32, P + 1), "split_spill" (f64, P + 1), "light_rank"
  * (u32, nl: the heavy rank j each light was paired with; its alias is

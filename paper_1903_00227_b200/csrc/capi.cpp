@@ -1085,12 +1085,15 @@ wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name, void* 
         } else if (nm == "heavy_w") {
             src = s->ws.hw;
             by = nh * 8;
-        } else if (nm == "light_prefix") {
-            src = s->ws.lpre;
-            by = (nl + 1) * 8;
-        } else if (nm == "heavy_prefix") {
-            src = s->ws.hpre;
-            by = (nh + 1) * 8;
+        } else if (nm == "light_prefix" || nm == "heavy_prefix") {
+            if (s->ws.ckpt)
+                return fail(WRS_EINVAL, "this build kept checkpointed prefixes (light_ckpt / heavy_ckpt)");
+            src = nm[0] == 'l' ? s->ws.lpre : s->ws.hpre;
+            by = ((nm[0] == 'l' ? nl : nh) + 1) * 8;
+        } else if (nm == "light_ckpt" || nm == "heavy_ckpt") {
+            if (!s->ws.ckpt) return fail(WRS_EINVAL, "this build kept full prefix arrays");
+            src = nm[0] == 'l' ? s->ws.lck : s->ws.hck;
+            by = ((nm[0] == 'l' ? nl : nh) + 15) / 16 * 16;  // one (hi, lo) pair per 16 items
         } else if (nm == "block_totals") {
             src = s->ws.totals;
             by = (nbl + nbh) * 8;

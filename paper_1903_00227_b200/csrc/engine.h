@@ -48,6 +48,9 @@ struct Workspace {
     double* hw = nullptr;            // gathered heavy weights
     double* lpre = nullptr;          // exclusive light prefix, nl + 1 entries
     double* hpre = nullptr;          // exclusive heavy prefix, nh + 1 entries
+    double2* lck = nullptr;          // (or) chain states before every 16th light ...
+    double2* hck = nullptr;          // ... and heavy: the checkpointed prefixes
+    bool ckpt = false;               // the last build kept checkpoints, not prefixes
     uint32_t* lrank = nullptr;       // K4a: alias heavy RANK of every light, list order
     double* hshare = nullptr;        // K4a: share of every heavy, list order
     uint32_t* lrank_own = nullptr;   // separate storage (else lrank aliases lpre)

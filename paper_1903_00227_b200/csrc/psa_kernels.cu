@@ -468,6 +468,96 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
     if (!PASS3 && me.len > 0) totals[b] = cs.value();  // carry[b] = local.value(), :114
 }
 
+// K2c, checkpoint form (large tables, W < 1e300): the same block chains as
+// k_scan_blocks<true>, but instead of every prefix value it keeps the chain's
+// state (hi, lo) BEFORE every 16th element of each block -- 1 B per item
+// instead of 8.  K3 only needs prefix values at its probe points, and any
+// prefix value is the state at the checkpoint at or before it plus at most
+// 16 more compensated adds (k_split_ckpt).  Checkpoint index = position / 16
+// (blocks are multiples of 16); the state at a block start is run.add(carry)
+// = (carry, 0) exactly (parallel.hpp:124).
+constexpr int CK_STRIDE = 16;
+__global__ void __launch_bounds__(K2_WARPS * 32)
+k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
+                   double2* __restrict__ lck, double2* __restrict__ hck, const DevScalars* sc,
+                   const double* __restrict__ carries) {
+    __shared__ double tile[K2_WARPS][2][32][K2_C + 1];
+    __shared__ K2Lane lanes[K2_WARPS][32];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t b = (static_cast<uint64_t>(blockIdx.x) * K2_WARPS + wq) * 32 + lane;
+
+    K2Lane me{nullptr, nullptr, 0};
+    double2* ck = nullptr;
+    if (b < nbl) {
+        me.src = lw + b * SCAN_BLOCK;
+        ck = lck + b * (SCAN_BLOCK / CK_STRIDE);
+        me.len = static_cast<int>(umin64(SCAN_BLOCK, nl - b * SCAN_BLOCK));
+    } else if (b - nbl < nbh) {
+        const uint64_t hb = b - nbl;
+        me.src = hw + hb * SCAN_BLOCK;
+        ck = hck + hb * (SCAN_BLOCK / CK_STRIDE);
+        me.len = static_cast<int>(umin64(SCAN_BLOCK, nh - hb * SCAN_BLOCK));
+    }
+    lanes[wq][lane] = me;
+    int maxlen = me.len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    if (maxlen == 0) return;
+    __syncwarp();
+
+    const int nchunks = (maxlen + K2_C - 1) / K2_C;
+    auto load_chunk = [&](int c, int buf) {
+#pragma unroll K2_ROW_U
+        for (int r = 0; r < 32; ++r) {
+            const K2Lane L = lanes[wq][r];
+            const int e = c * K2_C + lane;
+            if (e < L.len) cp_async8(&tile[wq][buf][r][lane], L.src + e);
+        }
+        cp_async_commit();
+    };
+
+    CompSumPos cs{0.0, 0.0};
+    if (me.len > 0) cs.add(carries[b]);  // run.add(carry[b]) = (carry, 0), parallel.hpp:124
+    load_chunk(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) {
+            load_chunk(c + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const int cnt = min(K2_C, me.len - c * K2_C);
+        const double* row = tile[wq][buf][lane];
+        if (cnt > 0) {
+            // the two checkpoints of this 32-element chunk: one full 32-B sector
+            double2 k0, k1;
+            k0 = make_double2(cs.hi, cs.lo);
+            if (cnt == K2_C) {
+#pragma unroll
+                for (int e = 0; e < CK_STRIDE; ++e) cs.add(row[e]);
+                k1 = make_double2(cs.hi, cs.lo);
+#pragma unroll
+                for (int e = CK_STRIDE; e < K2_C; ++e) cs.add(row[e]);
+            } else {
+                k1 = k0;
+                for (int e = 0; e < cnt; ++e) {
+                    if (e == CK_STRIDE) k1 = make_double2(cs.hi, cs.lo);
+                    cs.add(row[e]);
+                }
+            }
+            double2* d = ck + 2 * c;
+            __stcs(d, k0);
+            __stcs(d + 1, k1);
+        }
+        __syncwarp();
+    }
+}
+
 // Small tables (a few block chains per SM, so the chains' latency is the
 // kernel's time): one lane per block as above, but the block is read straight
 // into registers with 16-B loads, the next 32 elements in flight while the
@@ -985,6 +1075,100 @@ k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__
     split_s[k + 1] = spill;
 }
 
+// K3 over checkpointed prefixes (k_scan_blocks_ckpt): the same probe
+// sequence as k_split, each probe decided from a bracket first.  The prefix
+// value at x lies between the values of the checkpoints around it (prefix
+// values of non-negative terms only grow, up to rounding: each is within a
+// few ulps of the exact prefix sum), widened by 1e-13 relative; rounding is
+// monotone, so f(mid) = (L + H) + w lies between the same expressions of the
+// bracket ends.  Only when the target falls inside does the probe recompute
+// the exact L and H: the checkpoint state plus <= 16 compensated adds, the
+// additions k_scan_blocks<true> makes.  Results are identical to k_split's.
+struct CkList {
+    const double* w;    // the list's gathered weights
+    const double2* ck;  // states before every 16th element
+    uint64_t len;
+};
+__device__ __forceinline__ double ck_value(const CkList& L, uint64_t m) {
+    const double2 s = __ldg(L.ck + m);
+    return s.x + s.y;
+}
+// exact prefix value at x (alias.hpp:82-95: prefix[x] = out[x-1], prefix[0] = 0)
+__device__ __forceinline__ double ck_exact(const CkList& L, uint64_t x) {
+    if (x == 0) return 0.0;
+    const uint64_t e = x - 1;
+    const double2 s = __ldg(L.ck + (e / CK_STRIDE));
+    CompSumPos cs{s.x, s.y};
+    for (uint64_t p = e & ~static_cast<uint64_t>(CK_STRIDE - 1); p <= e; ++p) cs.add(__ldg(L.w + p));
+    return cs.value();
+}
+__device__ __forceinline__ void ck_bracket(const CkList& L, uint64_t x, double& lo, double& hi) {
+    if (x == 0) {
+        lo = hi = 0.0;
+        return;
+    }
+    const uint64_t m = (x - 1) / CK_STRIDE;
+    lo = ck_value(L, m) * (1.0 - 1e-13);
+    hi = (m + 1) * CK_STRIDE < L.len ? ck_value(L, m + 1) * (1.0 + 1e-13) : CUDART_INF;
+}
+
+__global__ void __launch_bounds__(256)
+k_split_ckpt(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__ lw,
+             const double* __restrict__ hw, const double2* __restrict__ lck,
+             const double2* __restrict__ hck, uint32_t* split_l, uint32_t* split_h,
+             double* split_s) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    if (nh == 0) return;  // uniform fill, K4
+    const double wn = sc->wn;
+    if (k == 0) {
+        split_l[0] = 0;
+        split_h[0] = 0;
+        split_s[0] = hw[0];  // carry of job 0 = w(heavy[0]), alias.hpp:219
+        split_l[P] = static_cast<uint32_t>(nl);
+        split_h[P] = static_cast<uint32_t>(nh);
+        split_s[P] = 0.0;
+    }
+    if (k + 1 >= P) return;
+    const CkList Lc{lw, lck, nl}, Hc{hw, hck, nh};
+    const uint64_t m = n * (k + 1);
+    const uint64_t np = m / P + (m % P != 0);  // alias.hpp:227
+    const double target = static_cast<double>(np) * wn;
+    uint64_t lo = np > nl ? np - nl : 0;
+    uint64_t hi = np < nh ? np : nh;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        bool above;  // f(mid) > target
+        if (mid >= nh) {
+            above = true;  // f = inf
+        } else {
+            const double w = __ldg(hw + mid);
+            double l0, l1, h0, h1;
+            ck_bracket(Lc, np - mid, l0, l1);
+            ck_bracket(Hc, mid, h0, h1);
+            if ((l0 + h0) + w > target) {
+                above = true;
+            } else if ((l1 + h1) + w <= target) {
+                above = false;
+            } else {
+                above = (ck_exact(Lc, np - mid) + ck_exact(Hc, mid)) + w > target;
+            }
+        }
+        if (above)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    double spill = 0.0;
+    if (lo < nh) {
+        const double x = (__ldg(hw + lo) + (ck_exact(Lc, np - lo) + ck_exact(Hc, lo))) - target;
+        spill = std_max(0.0, x);
+    }
+    split_l[k + 1] = static_cast<uint32_t>(np - lo);
+    split_h[k + 1] = static_cast<uint32_t>(lo);
+    split_s[k + 1] = spill;
+}
+
 // ===========================================================================
 // K4a: pack (psa_pack, alias.hpp:160-209) -- one lane per job
 //   Each lane runs its job's sequential compensated sweep (the remainder
@@ -1392,6 +1576,8 @@ cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate
     A(ws.hpre, n + 1);
     A(ws.totals, nblocks);
     A(ws.carries, nblocks);
+    A(ws.lck, n / CK_STRIDE + 2);
+    A(ws.hck, n / CK_STRIDE + 2);
     A(ws.split_l, P + 1);
     A(ws.split_h, P + 1);
     A(ws.split_s, P + 1);
@@ -1425,7 +1611,7 @@ void workspace_free(Workspace& ws) {
     void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.hidx,       ws.lw,
                     ws.hw,       ws.lpre,     ws.hpre,        ws.totals,
                     ws.carries,  ws.split_l,  ws.split_h,     ws.split_s,    ws.sc,
-                    ws.lrank_own, ws.hshare_own};
+                    ws.lrank_own, ws.hshare_own, ws.lck,       ws.hck};
     for (void* p : ptrs)
         if (p) dev_free(p);
     ws = Workspace{};
@@ -1483,6 +1669,13 @@ static int k2_direct_lpw(uint64_t nblocks) {
 static uint64_t k2_direct_max() {
     const char* e = std::getenv("WRS_B200_K2_DIRECT_MAX");  // read per build (tests flip it)
     return e ? std::strtoull(e, nullptr, 10) : (1ull << 25);
+}
+
+// Checkpointed prefixes for the staged K2 form (WRS_B200_K2_CKPT=0: full
+// prefix arrays, as the small-table forms always write).
+static bool k2_ckpt_enabled() {
+    const char* e = std::getenv("WRS_B200_K2_CKPT");
+    return !(e && e[0] == '0');
 }
 
 cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
@@ -1554,11 +1747,22 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     else
         k_scan_carry<CompSum><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     REC(3);
-    K2_LAUNCH(true);
+    // large tables: checkpoints instead of full prefix arrays (1 B per item
+    // written instead of 8; K3 recomputes what it probes)
+    ws.ckpt = pos && !split && !direct && k2_ckpt_enabled();
+    if (ws.ckpt)
+        k_scan_blocks_ckpt<<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lck, ws.hck, ws.sc,
+                                                              ws.carries);
+    else
+        K2_LAUNCH(true);
 #undef K2_LAUNCH
     REC(4);
-    k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l, ws.split_h,
-                                     ws.split_s);
+    if (ws.ckpt)
+        k_split_ckpt<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lw, ws.hw, ws.lck, ws.hck, ws.split_l,
+                                              ws.split_h, ws.split_s);
+    else
+        k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l,
+                                         ws.split_h, ws.split_s);
     REC(5);
     if (pos)  // W < 1e300: the remainder stays finite
         k_pack<true><<<k4_grid, k4_warps * 32, k4_smem, st>>>(

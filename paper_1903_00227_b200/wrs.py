@@ -349,7 +349,7 @@ class Sampler:
         dtypes = {"counts": np.uint64, "heavy": np.uint32, "light_rank": np.uint32,
                   "heavy_share": np.float64,
                   "light_w": np.float64, "heavy_w": np.float64, "light_prefix": np.float64,
-                  "heavy_prefix": np.float64, "block_totals": np.float64,
+                  "heavy_prefix": np.float64, "light_ckpt": np.float64, "heavy_ckpt": np.float64, "block_totals": np.float64,
                   "carries": np.float64, "split_light": np.uint32, "split_heavy": np.uint32,
                   "split_spill": np.float64}
         nbytes = u64()

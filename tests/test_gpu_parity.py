@@ -94,6 +94,33 @@ def test_golden_medium_generators_and_tables():
 
 # ---- per-stage parity ------------------------------------------------------------
 
+def check_checkpoints(ck, prefix, x):
+    """Checkpoint m holds the prefix chain's (hi, lo) state before element 16m
+    of the list (k_scan_blocks_ckpt): continuing the chain from it with the
+    same Neumaier adds (CompSumPos: all terms >= 0) must give exactly the
+    oracle's prefix values prefix[16m + 1 .. 16m + 16] (parallel.hpp:122-129),
+    stopping at block (2048) and list ends."""
+    n = x.size
+    m = ck.shape[0]
+    assert m == -(-n // 16)
+    hi, lo = ck[:, 0].copy(), ck[:, 1].copy()
+    base = np.arange(m) * 16
+    for e in range(16):
+        pos = base + e
+        live = (pos < n) & ((pos % 2048) >= (base % 2048))  # same block as the checkpoint
+        live &= (pos // 2048) == (base // 2048)
+        if not live.any():
+            break
+        xv = np.where(live, x[np.minimum(pos, n - 1)], 0.0)
+        t = hi + xv
+        big = hi >= xv
+        a = np.where(big, hi, xv)
+        b = np.where(big, xv, hi)
+        lo = np.where(live, lo + ((a - t) + b), lo)
+        hi = np.where(live, t, hi)
+        val = hi + lo
+        assert val[live].tobytes() == prefix[pos[live] + 1].tobytes(), e
+
 @pytest.mark.parametrize("k2", ["split", "direct", "direct-lpw1", "direct-lpw32", "staged"])
 def test_stages_bit_exact(P, k2, monkeypatch):
     # K2a/K2c have three forms (chains split over warps for a few blocks,
@@ -121,8 +148,13 @@ def test_stages_bit_exact(P, k2, monkeypatch):
             nbl = (part["light"].size + 2047) // 2048
             car = np.concatenate([P.scan_carries(tot[:nbl]), P.scan_carries(tot[nbl:])])
             assert S.stage("carries").tobytes() == car.tobytes()
-            assert S.stage("light_prefix").tobytes() == part["light_prefix"].tobytes()
-            assert S.stage("heavy_prefix").tobytes() == part["heavy_prefix"].tobytes()
+            if k2 == "staged":  # checkpointed prefixes (large-table form)
+                for name, pre, x in (("light_ckpt", part["light_prefix"], w[part["light"]]),
+                                     ("heavy_ckpt", part["heavy_prefix"], w[part["heavy"]])):
+                    check_checkpoints(S.stage(name).reshape(-1, 2), pre, x)
+            else:
+                assert S.stage("light_prefix").tobytes() == part["light_prefix"].tobytes()
+                assert S.stage("heavy_prefix").tobytes() == part["heavy_prefix"].tobytes()
             if nh:
                 bounds, spill = P.psa_plan(w, jobs)
                 sl, sh, ss = S.stage("split_light"), S.stage("split_heavy"), S.stage("split_spill")
