@@ -354,6 +354,82 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
     }
 }
 
+// K1, unstaged form (the default): the same tile classification and
+// look-back, but every thread keeps its 16 weights in registers and, once the
+// tile's list offsets are known, writes its lights / heavies straight to their
+// list positions (a warp row's lights, and its heavies, are consecutive
+// there).  No 40-KB staging buffer and one barrier less per tile; measured at
+// n = 1e8: 0.50 vs 0.53 ms for the staged form.
+__global__ void __launch_bounds__(K1_THREADS, 5)
+k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
+                   unsigned long long* status, double* __restrict__ lw, uint32_t* __restrict__ hidx,
+                   double* __restrict__ hw) {
+    __shared__ TileCells C;
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(&sc->tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * K1_TILE;
+    double xs[K1_ROWS];
+    classify_tile<true>(w, n, base, __ldcg(&sc->wn), xs, C);
+    if (warp == 0) {
+        const uint32_t totL = C.totL;
+        // decoupled look-back for the number of lights before this tile
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile(&status[0], FLAG_P | totL);
+        } else {
+            if (lane == 0) st_volatile(&status[tile], FLAG_A | totL);
+            long long p = static_cast<long long>(tile) - 1;
+            while (true) {
+                const long long idx = p - lane;
+                unsigned long long v = FLAG_P;
+                if (idx >= 0) {
+                    do {
+                        v = ld_volatile(&status[idx]);
+                    } while ((v >> 62) == 0);
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                unsigned long long c = v & VAL_MASK;
+                if (pm) {
+                    const int first = __ffs(pm) - 1;
+                    if (lane > first) c = 0;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                excl += c;
+                if (pm) break;
+                p -= 32;
+            }
+            if (lane == 0) st_volatile(&status[tile], FLAG_P | (excl + totL));
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if (tile + 1 == ntiles) {
+                sc->nl = excl + totL;
+                sc->nh = n - (excl + totL);
+            }
+        }
+    }
+    __syncthreads();
+    const uint64_t L0 = s_excl, H0 = base - s_excl;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const int cell = r * K1_WARPS + warp;
+        const unsigned lm = C.lm[cell], hm = C.hm[cell];
+        if ((lm >> lane) & 1) {
+            lw[L0 + C.exL[cell] + __popc(lm & lt)] = xs[r];
+        } else if ((hm >> lane) & 1) {
+            const uint64_t p = H0 + C.exH[cell] + __popc(hm & lt);
+            hidx[p] = static_cast<uint32_t>(base + r * K1_THREADS + tid);
+            hw[p] = xs[r];
+        }
+    }
+}
+
 // ===========================================================================
 // K2a / K2c: per-2048-block Neumaier chains, one lane per block
 // ===========================================================================
@@ -1671,6 +1747,12 @@ static uint64_t k2_direct_max() {
     return e ? std::strtoull(e, nullptr, 10) : (1ull << 25);
 }
 
+// K1 form: unstaged unless WRS_B200_K1=staged (tests run both)
+static bool k1_staged() {
+    const char* e = std::getenv("WRS_B200_K1");
+    return e && e[0] == 's';
+}
+
 // Checkpointed prefixes for the staged K2 form (WRS_B200_K2_CKPT=0: full
 // prefix arrays, as the small-table forms always write).
 static bool k2_ckpt_enabled() {
@@ -1711,8 +1793,12 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     e = cudaMemsetAsync(ws.tile_status, 0, ntiles * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     REC(0);
-    k_partition<<<static_cast<unsigned>(ntiles), K1_THREADS, k1_smem, st>>>(
-        d_w, n, ntiles, ws.sc, ws.tile_status, ws.lw, ws.hidx, ws.hw);
+    if (k1_staged())
+        k_partition<<<static_cast<unsigned>(ntiles), K1_THREADS, k1_smem, st>>>(
+            d_w, n, ntiles, ws.sc, ws.tile_status, ws.lw, ws.hidx, ws.hw);
+    else
+        k_partition_direct<<<static_cast<unsigned>(ntiles), K1_THREADS, 0, st>>>(
+            d_w, n, ntiles, ws.sc, ws.tile_status, ws.lw, ws.hidx, ws.hw);
     REC(1);
     // every prefix-chain value is finite and >= 0 when W is far below DBL_MAX
     const bool pos = total < 1e300;
