@@ -31,6 +31,8 @@ sys.path.insert(0, ROOT)
 
 N_ITEMS = 10**8
 K_SAMPLES = 10**9
+C2_ITEMS = 10**9    # BASELINE configs[2]
+C2_DRAWS = 10**10
 SEED = 42
 METRIC = "alias build Gitems/s + sample Gsamples/s at 1/2/4/8 B200; % HBM roofline"
 UNIT = "G(items+samples)/s"
@@ -54,6 +56,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-aggregate", action="store_true")
+    ap.add_argument("--c2-items", type=int, default=C2_ITEMS, help="configs[2] items in total")
+    ap.add_argument("--c2-draws", type=int, default=C2_DRAWS, help="configs[2] draws in total")
+    ap.add_argument("--no-config1", action="store_true", help="N > 1: skip configs[1] weak")
+    ap.add_argument("--no-config2", action="store_true", help="N = 1: skip configs[2]")
     return ap.parse_args()
 
 
@@ -264,11 +270,28 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # torchrun N>1: rank 0 alone runs the CPU arm
-    n, k = workload(args)
+    world = args.gpus
     import oracle
     oracle.build() if not os.path.exists(oracle.PORT_SO) else None
     R = oracle.ref()
-    w = (R or oracle.port()).generate_uniform(n, SEED)
+    if world == 1:
+        # configs[1] in full: n = 1e8 uniform, k = 1e9
+        n, k = workload(args)
+        w = (R or oracle.port()).generate_uniform(n, SEED)
+        cfg, scaling = config_obj(1), "weak"
+        data = "synthetic: reference generate_uniform(n, 42)"
+        sample = None
+    else:
+        # configs[2] (n = 1e9 power-law, k = 1e10) as a bounded sample: the
+        # reference's own generator at n = 1e8 and k = 1e9 per step (the
+        # full configuration takes ~35 s per step on 16 host threads); the
+        # metric is a rate, so the sample's rate stands for the whole
+        n, k = args.c2_items // 10, args.c2_draws // 10
+        w = (R or oracle.port()).generate_powerlaw(n, 1.0, SEED)
+        cfg, scaling = config_obj(2, world), "strong"
+        data = "synthetic: reference generate_powerlaw(1e8, 1.0, 42) (bounded sample of configs[2])"
+        sample = (f"bounded sample of configs[2]: AliasTable(generate_powerlaw({n}, 1.0, 42), "
+                  f"psa, T) + sample_many({k}) per step (the full n=1e9 / k=1e10 at this rate)")
     # one "step" = build + all k draws, median over the timed steps; the
     # warm-up steps run the same work untimed
     if args.warmup:
@@ -276,13 +299,14 @@ def run_reference(args):
     d = cpu_reference(n, k, max(1, args.steps), w=w)
     d.pop("w")
     value = (n + k) / d["step_s"] / 1e9
+    cb = cpu_baseline_obj(n, k, max(1, args.steps), d)
+    if sample:
+        cb["sample"] = sample
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": d["step_s"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: reference generate_uniform(n, 42)",
-        "config": config_obj(args, n, k),
-        "cpu_baseline": cpu_baseline_obj(n, k, max(1, args.steps), d),
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": data, "config": cfg, "cpu_baseline": cb,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -291,42 +315,104 @@ def workload(args) -> tuple[int, int]:
     return args.n, args.k
 
 
-def config_obj(args, n, k, world=1) -> dict:
+def config_obj(which: int, world: int = 1) -> dict:
     """The same keys in both arms (the driver compares them)."""
-    return {"workload": "BASELINE configs[1]: n=1e8 uniform(0,1] f64 per GPU, psa build + 1e9 "
-                        "with-replacement draws per GPU",
-            "n_per_gpu": n, "k_per_gpu": k,
-            "parallelism": f"shard{world}" if world > 1 else "single",
-            "l2": "no flush: weights 0.8 GB, table 1.6 GB, output 4 GB > 126 MB L2"}
+    if which == 1:
+        return {"workload": "BASELINE configs[1]: n=1e8 uniform(0,1] f64 per GPU, psa build + "
+                            "1e9 with-replacement draws per GPU",
+                "n_per_gpu": N_ITEMS, "k_per_gpu": K_SAMPLES,
+                "parallelism": f"shard{world}" if world > 1 else "single",
+                "l2": "no flush: weights 0.8 GB, table 1.6 GB, output 4 GB > 126 MB L2"}
+    return {"workload": "BASELINE configs[2]: n=1e9 power-law s=1 f64 (reference generator, "
+                        "shuffled, seed 42) sharded contiguously over the GPUs; per-shard psa "
+                        "tables + top table over the shard totals; 1e10 with-replacement draws "
+                        "split multinomially across the GPUs (strong scaling)",
+            "n_total": C2_ITEMS, "k_total": C2_DRAWS, "parallelism": f"shard{world}",
+            "l2": "no flush: weights 8 GB, tables 16 GB, output 40 GB in total > 126 MB L2"}
 
 
 # ------------------------------------------------------------- GPU arm
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
+class Ctx:
+    """What every GPU leg needs: torch, the library, the rank layout."""
 
-    import numpy as np
-    import torch
-    import torch.distributed as dist
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
 
-    import paper_1903_00227_b200 as wrs
+        import paper_1903_00227_b200 as wrs
+        self.args, self.torch, self.dist, self.wrs = args, torch, dist, wrs
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = os.environ.get("WRS_BENCH_BACKEND", "nccl")  # gloo: 1-GPU smoke of N>1
+        if self.backend != "nccl":
+            self.local %= torch.cuda.device_count()
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
+        self.dev = torch.device("cuda", self.local)
+        self.stream = torch.cuda.Stream(self.dev)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    backend = os.environ.get("WRS_BENCH_BACKEND", "nccl")  # gloo: 1-GPU smoke of the N>1 path
-    if backend != "nccl":
-        local %= torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.Stream(dev)
+    def timed(self, fn, reps):
+        """mean device ms of fn() on the stream, each call bracketed by events"""
+        torch = self.torch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps)]
+        torch.cuda.synchronize()
+        for a, b in evs:
+            with torch.cuda.stream(self.stream):
+                a.record(self.stream)
+                fn()
+                b.record(self.stream)
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs) / reps
 
+    def max_over_ranks(self, vals):
+        if self.world == 1:
+            return list(vals)
+        torch = self.torch
+        mdev = self.dev if self.backend == "nccl" else torch.device("cpu")
+        m = torch.tensor(list(vals), dtype=torch.float64, device=mdev)
+        self.dist.all_reduce(m, op=self.dist.ReduceOp.MAX)
+        return m.tolist()
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+
+def rooflines(n_local, k_local, build_ms, draw_ms):
+    hbm, hbm_kind = peaks()
+    tr = traffic_per_unit()
+    build_gbs = BUILD_BYTES_PER_ITEM * n_local / (build_ms * 1e-3) / 1e9
+    draw_gbs = SAMPLE_BYTES_PER_DRAW * k_local / (draw_ms * 1e-3) / 1e9
+
+    def traffic(key, units):
+        v = tr.get(key)
+        return None if v is None else v * units
+
+    build = {"gitems_per_s": n_local / (build_ms * 1e-3) / 1e9, "ms": build_ms,
+             "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": hbm,
+                          "peak_kind": hbm_kind, "unit": "GB/s", "frac": build_gbs / hbm,
+                          "bytes_per_item": BUILD_BYTES_PER_ITEM,
+                          "traffic": traffic("build_bytes_per_item", n_local)}}
+    draw = {"bound": "hbm",
+            "kernel": "draw stage: k_region_scatter + k_region_gather + k_region_unpermute",
+            "achieved": draw_gbs, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
+            "frac": draw_gbs / hbm, "bytes_per_sample": SAMPLE_BYTES_PER_DRAW,
+            "traffic": traffic("draw_bytes_per_sample", k_local)}
+    return build, draw
+
+
+def config1(ctx, weak_world: int):
+    """BASELINE configs[1] (n = 1e8 uniform, k = 1e9 per GPU).  weak_world > 1:
+    every rank owns a shard of weak_world * 1e8 items and draws its share of
+    weak_world * 1e9 (weak scaling; totals gathered with torch.distributed)."""
+    args, torch, wrs = ctx.args, ctx.torch, ctx.wrs
+    world, rank, stream = weak_world, ctx.rank, ctx.stream
     n_total, k_total = args.n * world, args.k * world
     lo, hi = wrs.shard_range(n_total, world, rank)
     W = wrs.Weights.generate_range("uniform", 0.0, n_total, lo, hi, SEED)
@@ -340,7 +426,7 @@ def main():
         shard = None
         S = wrs.Sampler.build(W, "psa", 1)
         cap = args.k
-    out = torch.empty(cap, dtype=torch.int32, device=dev)
+    out = torch.empty(cap, dtype=torch.int32, device=ctx.dev)
 
     def step():
         with torch.cuda.stream(stream):
@@ -349,31 +435,11 @@ def main():
             # runs on a side stream and overlaps the rebuild
             S.rebuild_async(stream)
             if shard is not None:
-                # the shard totals come with the weights (K0 at creation); a
-                # fresh job re-gathers them: one collective of G doubles
-                shard.totals = shard_gather(W.total())
-                k_me = shard.draw_device(SEED, k_total, out, stream)
-            else:
-                k_me = args.k
-                S.draw_device(SEED, k_me, 1, out, stream)
-        return k_me
-
-    def shard_gather(t):
-        from paper_1903_00227_b200.sharded import default_gather
-        return default_gather(t)
-
-    def timed(fn, reps):
-        """mean device ms of fn() on `stream`, each call bracketed by events"""
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(reps)]
-        torch.cuda.synchronize()
-        for a, b in evs:
-            with torch.cuda.stream(stream):
-                a.record(stream)
-                fn()
-                b.record(stream)
-        torch.cuda.synchronize()
-        return sum(a.elapsed_time(b) for a, b in evs) / reps
+                from paper_1903_00227_b200.sharded import default_gather
+                shard.totals = default_gather(W.total())
+                return shard.draw_device(SEED, k_total, out, stream)
+            S.draw_device(SEED, args.k, 1, out, stream)
+            return args.k
 
     for _ in range(args.warmup):
         step()
@@ -381,7 +447,7 @@ def main():
     S.check()
     # isolated halves for the rooflines (not the headline): build alone, the
     # per-kernel stage breakdown, draws alone against a fixed table
-    build_ms = timed(lambda: S.rebuild_async(stream), max(args.steps, 3))
+    build_ms = ctx.timed(lambda: S.rebuild_async(stream), max(args.steps, 3))
     wrs.set_timing(True)
     S.rebuild_async(stream)
     torch.cuda.synchronize()
@@ -389,80 +455,150 @@ def main():
     wrs.set_timing(False)
     S.rebuild_async(stream)  # re-arm the untimed path
     if shard is None:
-        draw_ms = timed(lambda: S.draw_device(SEED, args.k, 1, out, stream), max(args.steps, 3))
+        draw_ms = ctx.timed(lambda: S.draw_device(SEED, args.k, 1, out, stream), max(args.steps, 3))
     else:
-        draw_ms = timed(lambda: shard.draw_device(SEED, k_total, out, stream), max(args.steps, 3))
+        draw_ms = ctx.timed(lambda: shard.draw_device(SEED, k_total, out, stream),
+                            max(args.steps, 3))
     S.check()
 
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
-    k_drawn = 0
-    with ClockSampler(local) as clocks:
+    with ClockSampler(ctx.local) as clocks:
         t0.record(stream)
-        for i in range(args.steps):
-            k_drawn += step()
+        for _ in range(args.steps):
+            step()
         t1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     S.check()
-    ms = t0.elapsed_time(t1)
-    ms_step = ms / args.steps
-    if world > 1:  # max over ranks
-        mdev = dev if backend == "nccl" else torch.device("cpu")
-        m = torch.tensor([ms_step, build_ms, draw_ms], dtype=torch.float64, device=mdev)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        ms_step, build_ms, draw_ms = m.tolist()
-
-    hbm, hbm_kind = peaks()
-    k_per_rank = k_total / world
-    value = (n_total + k_total) / (ms_step * 1e-3) / 1e9
-    build_gbs = BUILD_BYTES_PER_ITEM * n_local / (build_ms * 1e-3) / 1e9
-    draw_gbs = SAMPLE_BYTES_PER_DRAW * k_per_rank / (draw_ms * 1e-3) / 1e9
-    tr = traffic_per_unit()
-
-    def traffic(key, units):
-        v = tr.get(key)
-        return None if v is None else v * units
-
-    result = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+    ms_step = t0.elapsed_time(t1) / args.steps
+    ms_step, build_ms, draw_ms = ctx.max_over_ranks([ms_step, build_ms, draw_ms])
+    build, draw_roof = rooflines(n_local, k_total / world, build_ms, draw_ms)
+    build["jobs"] = S.jobs
+    build["stages_ms"] = dict(zip(["K1_partition", "K2a_block_totals", "K2b_carries",
+                                   "K2c_prefix_checkpoints", "K3_splits", "K4a_pack",
+                                   "K4b_assemble"], [round(x, 4) for x in stage_ms]))
+    res = {
+        "value": (n_total + k_total) / (ms_step * 1e-3) / 1e9, "ms_per_step": ms_step,
+        "scaling": "weak", "config": config_obj(1, world),
         "data": "synthetic: reference generate_uniform(n_total, 42) generated on device",
-        "config": config_obj(args, args.n, args.k, world),
         "overlap": "each step = rebuild + draw; the draw's scatter (table-independent) runs on "
                    "a side stream concurrently with the rebuild; build/sample below are each "
                    "timed alone",
-        "build": {"gitems_per_s": n_local / (build_ms * 1e-3) / 1e9, "ms": build_ms,
-                  "jobs": S.jobs,
-                  "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": hbm,
-                               "peak_kind": hbm_kind, "unit": "GB/s", "frac": build_gbs / hbm,
-                               "bytes_per_item": BUILD_BYTES_PER_ITEM,
-                               "traffic": traffic("build_bytes_per_item", n_local)},
-                  "stages_ms": dict(zip(["K1_partition", "K2a_block_totals", "K2b_carries",
-                                         "K2c_prefixes", "K3_splits", "K4a_pack", "K4b_assemble"],
-                                        [round(x, 4) for x in stage_ms]))},
-        "sample": {"gsamples_per_s": k_per_rank / (draw_ms * 1e-3) / 1e9, "ms": draw_ms},
-        "roofline": {"bound": "hbm",
-                     "kernel": "draw stage: k_region_scatter + k_region_gather + k_region_unpermute",
-                     "achieved": draw_gbs, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
-                     "frac": draw_gbs / hbm, "bytes_per_sample": SAMPLE_BYTES_PER_DRAW,
-                     "traffic": traffic("draw_bytes_per_sample", k_per_rank)},
+        "build": build,
+        "sample": {"gsamples_per_s": k_total / world / (draw_ms * 1e-3) / 1e9, "ms": draw_ms},
+        "roofline": draw_roof,
         "gpu_launches": KERNELS_PER_STEP * args.steps,
         "clocks": clocks.summary(),
     }
+    del out, S, shard, W
+    torch.cuda.synchronize()
+    wrs.release_cache()
+    return res
+
+
+def config2(ctx):
+    """BASELINE configs[2]: n = 1e9 power-law s = 1 weights (the reference
+    generator: (i+1)^-1 dealt by its Fisher-Yates, seed 42), sharded
+    contiguously over the N ranks; k = 1e10 draws split multinomially across
+    the ranks -- strong scaling, the north star's multi-GPU target.  One step
+    = every rank rebuilds its shard table, the shard totals are all-gathered
+    over NCCL by the library (wrs_b200_multi_exchange), every rank derives
+    the same k-split and draws its share from its own table (global ids)."""
+    args, torch, wrs = ctx.args, ctx.torch, ctx.wrs
+    from paper_1903_00227_b200.sharded import multi_create
+    world, rank, stream = ctx.world, ctx.rank, ctx.stream
+    n_total, k_total = args.c2_items, args.c2_draws
+    lo, hi = wrs.shard_range(n_total, world, rank)
+    W = wrs.Weights.generate_range("powerlaw", 1.0, n_total, lo, hi, SEED)
+    wrs.release_cache()
+    M = multi_create(W, n_total, rank, world)
+    nccl = M.has_comm
+    counts = M.counts(SEED, k_total, world)
+    out = torch.empty(max(int(counts.max()), 1), dtype=torch.int32, device=ctx.dev)
+
+    def step():
+        with torch.cuda.stream(stream):
+            M.rebuild_async(stream)
+            if nccl:
+                M.exchange(stream)  # ncclAllGather of the G shard totals
+            return M.draw_device(SEED, k_total, out, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    M.sampler.check()
+    build_ms = ctx.timed(lambda: M.rebuild_async(stream), max(args.steps, 3))
+    draw_ms = ctx.timed(lambda: M.draw_device(SEED, k_total, out, stream), max(args.steps, 3))
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    torch.cuda.synchronize()
+    k_mine = 0
+    with ClockSampler(ctx.local) as clocks:
+        t0.record(stream)
+        for _ in range(args.steps):
+            k_mine += step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ctx.barrier()
+    M.sampler.check()
+    ms_step = t0.elapsed_time(t1) / args.steps
+    ms_step, build_ms, draw_ms = ctx.max_over_ranks([ms_step, build_ms, draw_ms])
+    build, draw_roof = rooflines(hi - lo, int(counts.max()), build_ms, draw_ms)
+    res = {
+        "value": (n_total + k_total) / (ms_step * 1e-3) / 1e9, "ms_per_step": ms_step,
+        "scaling": "strong", "config": config_obj(2, world),
+        "data": "synthetic: reference generate_powerlaw(1e9, 1.0, 42) (device deal, bit-exact)",
+        "exchange": "wrs_b200_multi_exchange: ncclAllGather of the shard totals (library-owned "
+                    "communicator)" if nccl else "totals gathered by torch.distributed",
+        "per_rank": {"items": hi - lo, "draws_max": int(counts.max()), "draws_min": int(counts.min()),
+                     "build_ms_max": build_ms, "draw_ms_max": draw_ms,
+                     "build": build, "draw_roofline": draw_roof},
+        "gpu_launches": (KERNELS_PER_STEP + 1) * args.steps,
+        "clocks": clocks.summary(),
+    }
+    del out
+    M.free()
+    W.free()
+    torch.cuda.synchronize()
+    wrs.release_cache()
+    return res
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    ctx = Ctx(args)
+    world, rank = ctx.world, ctx.rank
+    head = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "vs_baseline": None, "dtype": "f64"}
+    if world == 1:
+        # N = 1: BASELINE configs[1], the configuration the roofline targets
+        # are stated on; configs[2] on this one GPU is the strong-scaling
+        # curve's first point ("config2")
+        result = dict(head, **config1(ctx, 1))
+        if not args.no_config2:
+            result["config2"] = config2(ctx)
+    else:
+        # N > 1: BASELINE configs[2], strong scaling over the N ranks (the
+        # north star's multi-GPU target); configs[1] weak scaling beside it
+        result = dict(head, **config2(ctx))
+        if not args.no_config1:
+            result["config1_weak"] = config1(ctx, world)
+    lo, hi = ctx.wrs.shard_range(args.n * world, world, rank)
 
     # ---- aggregated draws (BASELINE configs[3] shape, on this GPU) ------------
     if world == 1 and not args.no_aggregate:
-        del out
-        result["aggregate"] = aggregate(args, wrs, torch, dev, stream)
+        result["aggregate"] = aggregate(args, ctx.wrs, ctx.torch, ctx.dev, ctx.stream)
 
     # ---- end to end through the C ABI with host buffers ---------------------
     if not args.no_e2e:
-        result["e2e"] = e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total)
+        if world == 1:
+            result["e2e"] = e2e(args, ctx.wrs, ctx.torch, world, rank, lo, hi, args.n, args.k)
+        else:
+            result["e2e"] = e2e_multi(ctx)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         # the reference on this host's cores: 3 builds + 3 full k-draw runs
@@ -471,10 +607,56 @@ def main():
         d.pop("w")
         result["cpu_baseline"] = cpu_baseline_obj(args.n, args.k, 3, d)
     if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        ctx.dist.barrier()
+        ctx.dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result))
+
+
+def e2e_multi(ctx):
+    """configs[2] end to end at N ranks through the public API with host
+    buffers: every step each rank copies its shard of the weights from pinned
+    host memory (wrs_weights_from_array), builds its multi-GPU handle (shard
+    table; the totals gathered with the caller's process group), draws its
+    share of k and copies it back to pinned host memory.  Max over ranks."""
+    args, torch, wrs = ctx.args, ctx.torch, ctx.wrs
+    from paper_1903_00227_b200.sharded import default_gather
+    world, rank = ctx.world, ctx.rank
+    n_total, k_total = args.c2_items, args.c2_draws
+    lo, hi = wrs.shard_range(n_total, world, rank)
+    Wd = wrs.Weights.generate_range("powerlaw", 1.0, n_total, lo, hi, SEED)
+    host_w = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True)
+    host_w.numpy()[:] = Wd.values()
+    totals = default_gather(Wd.total())
+    Wd.free()
+    wrs.release_cache()
+    cnt = int(wrs.shard_counts(totals, SEED, k_total)[rank])
+    host_out = torch.empty(max(cnt, 1), dtype=torch.int32, pin_memory=True)
+    dev_out = torch.empty(max(cnt, 1), dtype=torch.int32, device=ctx.dev)
+    times = []
+    for i in range(1 + max(1, min(args.steps, 3))):
+        ctx.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        W = wrs.Weights.from_array(host_w.numpy())
+        M = wrs.MultiSampler.create(W, n_total, rank, world, None)
+        M.set_totals(default_gather(W.total()))
+        M.draw_device(SEED, k_total, dev_out, ctx.stream)
+        with torch.cuda.stream(ctx.stream):
+            host_out.copy_(dev_out, non_blocking=True)
+        ctx.stream.synchronize()
+        checksum = int(host_out[-1])
+        t1 = time.perf_counter()
+        M.free()
+        W.free()
+        if i:
+            times.append(t1 - t0)
+    sec = ctx.max_over_ranks([statistics.median(times)])[0]
+    return {"value": (n_total + k_total) / sec / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": 8 * (hi - lo), "d2h_bytes_per_step": 4 * cnt,
+            "ms_per_step": sec * 1e3,
+            "api": "wrs_weights_from_array + wrs_b200_multi_create/set_totals + "
+                   "wrs_b200_multi_draw_device + D2H", "checksum_last": checksum}
 
 
 def aggregate(args, wrs, torch, dev, stream):

@@ -157,6 +157,60 @@ WRS_API wrs_status wrs_b200_sampler_draw_shard_device(const wrs_sampler* s, uint
                                                       uint64_t base, uint32_t* d_out,
                                                       void* stream);
 
+/* -------------------------------------------- multi-GPU sampler (NCCL)
+ * One rank per GPU (one process each, or G handles in one process): rank g
+ * owns the contiguous shard [g*ceil(n/G), min(n, (g+1)*ceil(n/G))) of the
+ * global weight vector (two_level.hpp:33-41), builds its PSA table, and the
+ * ranks all-gather their shard totals (each the shard's bit-exact pairwise
+ * sum, two_level.hpp:49-51) with one ncclAllGather of G doubles, device to
+ * device, over NVLink.  Every rank then builds the same top table over the
+ * totals (two_level.hpp:56-57) and derives the same per-rank draw counts for
+ * (seed, k) with the communication-free binomial descent
+ * (wrs_b200_shard_counts); each rank draws its count from its own table and
+ * writes global ids.  The library owns the NCCL communicator; NCCL itself
+ * (libnccl.so.2) is loaded at the first multi call, so single-GPU users never
+ * need it. */
+typedef struct wrs_b200_multi wrs_b200_multi;
+/* 1 if libnccl.so.2 can be loaded (its version in *version, may be NULL). */
+WRS_API int wrs_b200_nccl_available(int* version);
+/* A new NCCL unique id (128 bytes) for one job: rank 0 creates it, the
+ * caller hands it to every rank. */
+WRS_API wrs_status wrs_b200_nccl_unique_id(void* id128);
+/* Rank `rank` of `ranks`: `shard` holds this rank's items (on the current
+ * device).  With nccl_id != NULL the communicator is created
+ * (ncclCommInitRank, collective over all ranks) and the totals exchanged;
+ * with nccl_id == NULL the caller supplies the gathered totals with
+ * wrs_b200_multi_set_totals (its own collective). */
+WRS_API wrs_status wrs_b200_multi_create(const wrs_weights* shard, uint64_t n_total,
+                                         uint32_t rank, uint32_t ranks, const void* nccl_id,
+                                         wrs_b200_multi** out);
+/* All G ranks in this process, shards[g] on its own device (distinct
+ * devices): one ncclCommInitAll, then every rank's exchange in one group. */
+WRS_API wrs_status wrs_b200_multi_create_local(const wrs_weights* const* shards, uint32_t ranks,
+                                               uint64_t n_total, wrs_b200_multi** out);
+WRS_API wrs_status wrs_b200_multi_set_totals(wrs_b200_multi* m, const double* totals);
+/* Re-exchange the totals (ncclAllGather on `stream`, device to device; the
+ * host copy is read back before returning).  Collective. */
+WRS_API wrs_status wrs_b200_multi_exchange(wrs_b200_multi* m, void* stream);
+/* Rebuild this rank's shard table on `stream` (wrs_b200_sampler_rebuild_async). */
+WRS_API wrs_status wrs_b200_multi_rebuild_async(wrs_b200_multi* m, void* stream);
+WRS_API wrs_status wrs_b200_multi_totals(const wrs_b200_multi* m, double* totals);
+/* counts[0..ranks) for (seed, k), identical on every rank. */
+WRS_API wrs_status wrs_b200_multi_counts(const wrs_b200_multi* m, uint64_t seed, uint64_t k,
+                                         uint64_t* counts);
+/* This rank's draws of the k-draw job (global ids) into d_out, asynchronous
+ * on `stream`; *count gets how many (counts[rank]).  The same values as
+ * wrs_b200_sampler_draw_shard_device(shard table, seed, rank, count, lo). */
+WRS_API wrs_status wrs_b200_multi_draw_device(const wrs_b200_multi* m, uint64_t seed,
+                                              uint64_t k, uint32_t* d_out, void* stream,
+                                              uint64_t* count);
+/* The top table over the gathered totals (ranks 16-B buckets) and its mean. */
+WRS_API wrs_status wrs_b200_multi_top_buckets(const wrs_b200_multi* m, void* host_out,
+                                              double* bucket_mean);
+/* This rank's shard sampler (owned by the handle; do not free). */
+WRS_API const wrs_sampler* wrs_b200_multi_shard(const wrs_b200_multi* m);
+WRS_API void wrs_b200_multi_free(wrs_b200_multi* m);
+
 /* ------------------------------------------ routed two-level draws (§8f 2)
  * TwoLevelTable::sample_many(seed, k, workers) (two_level.hpp:66-81),
  * outputs [q_begin, q_end) into d_out[0 .. q_end - q_begin): per query the

@@ -7,6 +7,8 @@
 // WRS_ENOMEM (allocation) or WRS_EINTERNAL.  There is no CPU compute path:
 // a missing or unusable GPU makes every compute call fail loudly.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed by the multi-GPU calls
 
 #include <algorithm>
 #include <atomic>
@@ -21,6 +23,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "engine.h"
@@ -1122,5 +1125,265 @@ wrs_status wrs_b200_sampler_stage(const wrs_sampler* s, const char* name, void* 
         return WRS_OK;
     });
 }
+
+
+// ---- multi-GPU sampler (NCCL) ------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+// NCCL, loaded on first use (libnccl.so.2: the copy already in the process,
+// e.g. PyTorch's, else the system one).
+struct Nccl {
+    bool ok = false;
+    int version = 0;
+    std::string err;
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommInitAll) commInitAll = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclGetVersion) getVersion = nullptr;
+};
+
+Nccl& nccl() {
+    static Nccl n = [] {
+        Nccl x;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            x.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return x;
+        }
+        auto sym = [&](auto& f, const char* name) {
+            f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+            return f != nullptr;
+        };
+        x.ok = sym(x.getUniqueId, "ncclGetUniqueId") && sym(x.commInitRank, "ncclCommInitRank") &&
+               sym(x.commInitAll, "ncclCommInitAll") && sym(x.allGather, "ncclAllGather") &&
+               sym(x.commDestroy, "ncclCommDestroy") && sym(x.errorString, "ncclGetErrorString") &&
+               sym(x.groupStart, "ncclGroupStart") && sym(x.groupEnd, "ncclGroupEnd") &&
+               sym(x.getVersion, "ncclGetVersion");
+        if (!x.ok)
+            x.err = "libnccl.so.2 lacks a needed symbol";
+        else
+            x.getVersion(&x.version);
+        return x;
+    }();
+    return n;
+}
+
+Nccl& need_nccl() {
+    Nccl& n = nccl();
+    if (!n.ok) throw std::runtime_error(n.err);
+    return n;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + nccl().errorString(r));
+}
+
+}  // namespace
+
+struct wrs_b200_multi {
+    std::unique_ptr<wrs_sampler> shard;
+    uint32_t rank = 0, ranks = 1;
+    uint64_t n_total = 0, lo = 0, hi = 0;
+    int device = 0;
+    ncclComm_t comm = nullptr;
+    std::unique_ptr<DevBuf> d_total, d_totals;  // this shard's total, the gathered totals
+    std::vector<double> totals;
+    std::shared_ptr<WeightsData> top_w;
+    std::unique_ptr<wrs_sampler> top;
+    ~wrs_b200_multi() {
+        if (device >= 0) cudaSetDevice(device);
+        top.reset();
+        if (comm && nccl().ok) nccl().commDestroy(comm);
+    }
+};
+
+namespace {
+
+std::unique_ptr<wrs_b200_multi> multi_new(const wrs_weights* shard, uint64_t n_total, uint32_t rank,
+                                          uint32_t ranks) {
+    if (ranks == 0 || rank >= ranks) throw std::invalid_argument("rank must be < ranks");
+    auto m = std::make_unique<wrs_b200_multi>();
+    m->rank = rank;
+    m->ranks = ranks;
+    m->n_total = n_total;
+    wrs_b200_shard_range(n_total, ranks, rank, &m->lo, &m->hi);
+    if (shard->data->n != m->hi - m->lo)
+        throw std::invalid_argument("shard holds " + std::to_string(shard->data->n) +
+                                    " items, rank " + std::to_string(rank) + " owns " +
+                                    std::to_string(m->hi - m->lo));
+    m->device = shard->data->device;
+    ck(cudaSetDevice(m->device), "cudaSetDevice");
+    m->shard = build_psa(shard->data, wrsb::default_jobs(shard->data->n), 0, "psa");
+    m->d_total = std::make_unique<DevBuf>(sizeof(double));
+    m->d_totals = std::make_unique<DevBuf>(ranks * sizeof(double));
+    ck(cudaMemcpy(m->d_total->p, &shard->data->total, sizeof(double), cudaMemcpyHostToDevice),
+       "total H2D");
+    return m;
+}
+
+// the top table over the gathered totals (two_level.hpp:56-57)
+void multi_set_totals(wrs_b200_multi& m, const double* totals) {
+    ck(cudaSetDevice(m.device), "cudaSetDevice");
+    const bool same = m.totals.size() == m.ranks &&
+                      std::memcmp(m.totals.data(), totals, m.ranks * sizeof(double)) == 0;
+    if (same && m.top) return;
+    m.totals.assign(totals, totals + m.ranks);
+    m.top.reset();
+    m.top_w = weights_from_host(m.totals.data(), m.ranks);
+    m.top = build_psa(m.top_w, wrsb::default_jobs(m.ranks), 0, "psa");
+}
+
+void multi_read_totals(wrs_b200_multi& m, cudaStream_t st) {
+    std::vector<double> t(m.ranks);
+    ck(cudaMemcpyAsync(t.data(), m.d_totals->p, m.ranks * sizeof(double), cudaMemcpyDeviceToHost, st),
+       "totals D2H");
+    ck(cudaStreamSynchronize(st), "totals");
+    multi_set_totals(m, t.data());
+}
+
+}  // namespace
+
+extern "C" {
+
+int wrs_b200_nccl_available(int* version) {
+    Nccl& n = nccl();
+    if (version) *version = n.ok ? n.version : 0;
+    return n.ok ? 1 : 0;
+}
+
+wrs_status wrs_b200_nccl_unique_id(void* id128) {
+    if (!id128) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        ncclUniqueId id;
+        nck(need_nccl().getUniqueId(&id), "ncclGetUniqueId");
+        static_assert(sizeof id == 128, "NCCL unique id is 128 bytes");
+        std::memcpy(id128, &id, sizeof id);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_multi_create(const wrs_weights* shard, uint64_t n_total, uint32_t rank,
+                                 uint32_t ranks, const void* nccl_id, wrs_b200_multi** out) {
+    if (!shard || !out) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        auto m = multi_new(shard, n_total, rank, ranks);
+        if (nccl_id) {
+            Nccl& n = need_nccl();
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof id);
+            nck(n.commInitRank(&m->comm, static_cast<int>(ranks), id, static_cast<int>(rank)),
+                "ncclCommInitRank");
+            nck(n.allGather(m->d_total->p, m->d_totals->p, 1, ncclFloat64, m->comm,
+                            m->shard->stream->s),
+                "ncclAllGather");
+            multi_read_totals(*m, m->shard->stream->s);
+        }
+        *out = m.release();
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_multi_create_local(const wrs_weights* const* shards, uint32_t ranks,
+                                       uint64_t n_total, wrs_b200_multi** out) {
+    if (!shards || !out || ranks == 0) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        Nccl& n = need_nccl();
+        std::vector<std::unique_ptr<wrs_b200_multi>> ms;
+        std::vector<int> devs;
+        for (uint32_t g = 0; g < ranks; ++g) {
+            if (!shards[g]) throw std::invalid_argument("null shard");
+            ms.push_back(multi_new(shards[g], n_total, g, ranks));
+            devs.push_back(ms.back()->device);
+        }
+        std::vector<ncclComm_t> comms(ranks);
+        nck(n.commInitAll(comms.data(), static_cast<int>(ranks), devs.data()), "ncclCommInitAll");
+        for (uint32_t g = 0; g < ranks; ++g) ms[g]->comm = comms[g];
+        nck(n.groupStart(), "ncclGroupStart");
+        for (uint32_t g = 0; g < ranks; ++g) {
+            ck(cudaSetDevice(ms[g]->device), "cudaSetDevice");
+            nck(n.allGather(ms[g]->d_total->p, ms[g]->d_totals->p, 1, ncclFloat64, ms[g]->comm,
+                            ms[g]->shard->stream->s),
+                "ncclAllGather");
+        }
+        nck(n.groupEnd(), "ncclGroupEnd");
+        for (uint32_t g = 0; g < ranks; ++g) multi_read_totals(*ms[g], ms[g]->shard->stream->s);
+        for (uint32_t g = 0; g < ranks; ++g) out[g] = ms[g].release();
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_multi_set_totals(wrs_b200_multi* m, const double* totals) {
+    if (!m || !totals) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        multi_set_totals(*m, totals);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_multi_exchange(wrs_b200_multi* m, void* stream) {
+    if (!m) return fail(WRS_EINVAL, "null argument");
+    return guarded([&] {
+        if (!m->comm) throw std::invalid_argument("handle has no NCCL communicator");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : m->shard->stream->s;
+        nck(need_nccl().allGather(m->d_total->p, m->d_totals->p, 1, ncclFloat64, m->comm, st),
+            "ncclAllGather");
+        multi_read_totals(*m, st);
+        return WRS_OK;
+    });
+}
+
+wrs_status wrs_b200_multi_rebuild_async(wrs_b200_multi* m, void* stream) {
+    if (!m) return fail(WRS_EINVAL, "null argument");
+    return wrs_b200_sampler_rebuild_async(m->shard.get(), stream);
+}
+
+wrs_status wrs_b200_multi_totals(const wrs_b200_multi* m, double* totals) {
+    if (!m || !totals) return fail(WRS_EINVAL, "null argument");
+    if (m->totals.size() != m->ranks) return fail(WRS_EINVAL, "totals not exchanged yet");
+    std::memcpy(totals, m->totals.data(), m->ranks * sizeof(double));
+    return WRS_OK;
+}
+
+wrs_status wrs_b200_multi_counts(const wrs_b200_multi* m, uint64_t seed, uint64_t k,
+                                 uint64_t* counts) {
+    if (!m || !counts) return fail(WRS_EINVAL, "null argument");
+    if (m->totals.size() != m->ranks) return fail(WRS_EINVAL, "totals not exchanged yet");
+    return wrs_b200_shard_counts(m->totals.data(), m->ranks, seed, k, counts);
+}
+
+wrs_status wrs_b200_multi_draw_device(const wrs_b200_multi* m, uint64_t seed, uint64_t k,
+                                      uint32_t* d_out, void* stream, uint64_t* count) {
+    if (!m || !count) return fail(WRS_EINVAL, "null argument");
+    if (m->totals.size() != m->ranks) return fail(WRS_EINVAL, "totals not exchanged yet");
+    return guarded([&]() -> wrs_status {
+        std::vector<uint64_t> c(m->ranks);
+        const wrs_status r = wrs_b200_shard_counts(m->totals.data(), m->ranks, seed, k, c.data());
+        if (r != WRS_OK) return r;
+        *count = c[m->rank];
+        if (!d_out && *count) return fail(WRS_EINVAL, "null output");
+        return wrs_b200_sampler_draw_shard_device(m->shard.get(), seed, m->rank, *count, m->lo,
+                                                  d_out, stream);
+    });
+}
+
+wrs_status wrs_b200_multi_top_buckets(const wrs_b200_multi* m, void* host_out, double* bucket_mean) {
+    if (!m || !host_out) return fail(WRS_EINVAL, "null argument");
+    if (!m->top) return fail(WRS_EINVAL, "totals not exchanged yet");
+    if (bucket_mean) *bucket_mean = m->top->wn;
+    return wrs_b200_sampler_copy_buckets(m->top.get(), host_out);
+}
+
+const wrs_sampler* wrs_b200_multi_shard(const wrs_b200_multi* m) { return m ? m->shard.get() : nullptr; }
+
+void wrs_b200_multi_free(wrs_b200_multi* m) { delete m; }
 
 }  // extern "C"

@@ -131,3 +131,36 @@ class ShardedSampler:
         for p in getattr(self, "_opened", []):
             _w.ipc_close(p)
         self._opened = []
+
+
+# ---- the C++-owned multi-GPU sampler (wrs_b200_multi_*) ---------------------------
+def job_nccl_id(rank: int, world: int) -> bytes:
+    """The job's NCCL unique id: made by rank 0 (wrs_b200_nccl_unique_id),
+    broadcast to every rank over torch.distributed."""
+    import torch.distributed as dist
+    nid = [_w.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(nid, src=0)
+    return nid[0]
+
+
+def multi_create(weights: "_w.Weights", n_total: int, rank: int, world: int,
+                 use_nccl: bool | None = None) -> "_w.MultiSampler":
+    """This rank's wrs_b200_multi handle.  With NCCL (the default when
+    libnccl.so.2 loads and torch.distributed runs the nccl backend) rank 0
+    makes the job's NCCL unique id, torch.distributed broadcasts those 128
+    bytes, and the library creates its own communicator and all-gathers the
+    shard totals device to device.  Otherwise (gloo, CPU tests) the totals
+    are gathered with torch.distributed and handed to the library."""
+    import torch.distributed as dist
+    if use_nccl is None:
+        use_nccl = _w.nccl_available()[0] and (world == 1 or dist.get_backend() == "nccl")
+    if use_nccl:
+        m = _w.MultiSampler.create(weights, n_total, rank, world, job_nccl_id(rank, world))
+        m.has_comm = True
+        return m
+    m = _w.MultiSampler.create(weights, n_total, rank, world, None)
+    m.has_comm = False
+    m.set_totals(default_gather(weights.total()) if world > 1 else [weights.total()])
+    return m
+

@@ -84,6 +84,19 @@ SIGNATURES = {
     "wrs_b200_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
     "wrs_b200_ipc_close": (C.c_int, [vp]),
     "wrs_b200_sampler_draw_counts_device": (C.c_int, [vp, u64, u64, C.c_uint, vp, vp, vp, vp]),
+    "wrs_b200_nccl_available": (C.c_int, [C.POINTER(C.c_int)]),
+    "wrs_b200_nccl_unique_id": (C.c_int, [vp]),
+    "wrs_b200_multi_create": (C.c_int, [vp, u64, u32, u32, vp, C.POINTER(vp)]),
+    "wrs_b200_multi_create_local": (C.c_int, [vp, u32, u64, vp]),
+    "wrs_b200_multi_set_totals": (C.c_int, [vp, vp]),
+    "wrs_b200_multi_exchange": (C.c_int, [vp, vp]),
+    "wrs_b200_multi_rebuild_async": (C.c_int, [vp, vp]),
+    "wrs_b200_multi_totals": (C.c_int, [vp, vp]),
+    "wrs_b200_multi_counts": (C.c_int, [vp, u64, u64, vp]),
+    "wrs_b200_multi_draw_device": (C.c_int, [vp, u64, u64, vp, vp, C.POINTER(u64)]),
+    "wrs_b200_multi_top_buckets": (C.c_int, [vp, vp, C.POINTER(f64)]),
+    "wrs_b200_multi_shard": (vp, [vp]),
+    "wrs_b200_multi_free": (None, [vp]),
 }
 
 _lib = None
@@ -368,6 +381,95 @@ class Sampler:
     def free(self) -> None:
         if self.h:
             lib().wrs_sampler_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def nccl_available() -> tuple[bool, int]:
+    """(libnccl.so.2 loadable, its version code)."""
+    v = C.c_int()
+    return bool(lib().wrs_b200_nccl_available(C.byref(v))), v.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().wrs_b200_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class _BorrowedSampler(Sampler):
+    """A sampler handle owned by something else (never freed here)."""
+
+    def free(self) -> None:
+        self.h = None
+
+
+class MultiSampler:
+    """wrs_b200_multi handle: one rank's part of the C++-owned multi-GPU
+    sampler (shard table, NCCL all-gather of the shard totals, top table,
+    binomial k-split, this rank's draws with global ids)."""
+
+    def __init__(self, handle, shard: "Weights"):
+        self.h = handle
+        self.shard_weights = shard
+        self.sampler = _BorrowedSampler(lib().wrs_b200_multi_shard(handle), shard)
+
+    @classmethod
+    def create(cls, shard: "Weights", n_total: int, rank: int, ranks: int,
+               nccl_id: bytes | None) -> "MultiSampler":
+        h = vp()
+        idp = C.c_char_p(nccl_id) if nccl_id is not None else None
+        _check(lib().wrs_b200_multi_create(shard.h, n_total, rank, ranks, idp, C.byref(h)))
+        return cls(h, shard)
+
+    @classmethod
+    def create_local(cls, shards: list, n_total: int) -> list:
+        G = len(shards)
+        hs = (vp * G)(*[w.h for w in shards])
+        out = (vp * G)()
+        _check(lib().wrs_b200_multi_create_local(hs, G, n_total, out))
+        return [cls(vp(out[g]), shards[g]) for g in range(G)]
+
+    def set_totals(self, totals) -> None:
+        t = np.ascontiguousarray(totals, np.float64)
+        _check(lib().wrs_b200_multi_set_totals(self.h, _ptr(t)))
+
+    def exchange(self, stream=None) -> None:
+        _check(lib().wrs_b200_multi_exchange(self.h, _stream_ptr(stream)))
+
+    def rebuild_async(self, stream=None) -> None:
+        _check(lib().wrs_b200_multi_rebuild_async(self.h, _stream_ptr(stream)))
+
+    def totals(self, ranks: int) -> np.ndarray:
+        out = np.empty(ranks, np.float64)
+        _check(lib().wrs_b200_multi_totals(self.h, _ptr(out)))
+        return out
+
+    def counts(self, seed: int, k: int, ranks: int) -> np.ndarray:
+        out = np.empty(ranks, np.uint64)
+        _check(lib().wrs_b200_multi_counts(self.h, seed, k, _ptr(out)))
+        return out
+
+    def draw_device(self, seed: int, k: int, out, stream=None) -> int:
+        c = u64()
+        _check(lib().wrs_b200_multi_draw_device(self.h, seed, k, _dev_ptr(out),
+                                                _stream_ptr(stream, out), C.byref(c)))
+        return c.value
+
+    def top_buckets(self, ranks: int) -> tuple[np.ndarray, float]:
+        out = np.empty(ranks, BUCKET_DTYPE)
+        m = f64()
+        _check(lib().wrs_b200_multi_top_buckets(self.h, _ptr(out), C.byref(m)))
+        return out, m.value
+
+    def free(self) -> None:
+        if self.h:
+            lib().wrs_b200_multi_free(self.h)
             self.h = None
 
     def __del__(self):

@@ -143,3 +143,27 @@ def test_compute_calls_fail_loudly_without_gpu():
     with pytest.raises(wrs.WrsError) as e:
         wrs.Weights.from_array(np.array([1.0, 2.0]))
     assert e.value.status in (wrs.wrs.WRS_EINTERNAL, wrs.wrs.WRS_ENOMEM)
+
+
+def test_nccl_loads_lazily_for_the_multi_gpu_path():
+    """libwrs_b200.so has no link-time NCCL dependency; the multi-GPU calls
+    dlopen libnccl.so.2 (here: the system NCCL) and can make a job's unique
+    id without a GPU."""
+    import subprocess
+    deps = subprocess.run(["ldd", wrs.wrs.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nccl" not in deps
+    ok, version = wrs.nccl_available()
+    assert ok and version >= 22700, version
+    a, b = wrs.nccl_unique_id(), wrs.nccl_unique_id()
+    assert len(a) == 128 and a != b
+
+
+def test_multi_calls_validate_arguments():
+    L = lib()
+    h = C.c_void_p()
+    assert L.wrs_b200_multi_create(None, 10, 0, 1, None, C.byref(h)) == wrs.wrs.WRS_EINVAL
+    assert L.wrs_b200_multi_set_totals(None, None) == wrs.wrs.WRS_EINVAL
+    assert L.wrs_b200_multi_exchange(None, None) == wrs.wrs.WRS_EINVAL
+    assert L.wrs_b200_multi_counts(None, 1, 1, None) == wrs.wrs.WRS_EINVAL
+    assert L.wrs_b200_multi_shard(None) is None
+    L.wrs_b200_multi_free(None)

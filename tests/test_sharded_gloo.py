@@ -69,3 +69,30 @@ def test_sharded_counts_agree_across_ranks(tmp_path, world):
         from tests.test_capi_host import _replay_counts
         assert list(res[0]["counts"]) == _replay_counts(R, oracle.port(), list(res[0]["totals"]),
                                                         seed, k)
+
+
+def _id_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1903_00227_b200.sharded import job_nccl_id
+    nid = job_nccl_id(rank, world)
+    with open(os.path.join(out_dir, f"id{rank}.bin"), "wb") as f:
+        f.write(nid)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_multi_gpu_job_shares_one_nccl_id(tmp_path):
+    """bench.py's N > 1 path (sharded.multi_create): rank 0 makes the job's
+    NCCL unique id through the library, the process group broadcasts it, and
+    every rank hands the same 128 bytes to wrs_b200_multi_create."""
+    import paper_1903_00227_b200 as wrs
+    if not wrs.nccl_available()[0]:
+        pytest.skip("libnccl.so.2 not loadable")
+    world = 2
+    mp.spawn(_id_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    ids = [(tmp_path / f"id{r}.bin").read_bytes() for r in range(world)]
+    assert len(ids[0]) == 128 and all(x == ids[0] for x in ids)
+
