@@ -664,9 +664,7 @@ def aggregate(args, wrs, torch, dev, stream):
     aggregated to (item, count) pairs (wrs_b200_sampler_draw_counts_device):
     the same alias draws as the main line, counted instead of written."""
     n, k = args.n, args.k
-    g = torch.Generator(device=dev).manual_seed(SEED)
-    wt = torch.exp(2.0 * torch.randn(n, dtype=torch.float64, device=dev, generator=g))
-    W = wrs.Weights.from_device(wt)
+    W = wrs.Weights.generate("lognormal", 2.0, n, SEED)  # common.cuh, restated in the oracle
     S = wrs.Sampler.build(W, "psa", 1)
     cap = min(n, k)
     items = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -686,7 +684,8 @@ def aggregate(args, wrs, torch, dev, stream):
     nu = int(m.item())
     assert int(counts[:nu].sum()) == k
     return {"workload": "BASELINE configs[3] on 1 GPU: n=%d lognormal(0,2) f64 weights "
-                        "(torch cuda generator, seed %d), k=%d draws -> (item, count) pairs"
+                        "(the library's Box-Muller generator on RngStream(seed, 'logn'), seed %d; "
+                        "oracle twin wo_generate_lognormal), k=%d draws -> (item, count) pairs"
                         % (n, SEED, k),
             "gsamples_per_s": k / (ms * 1e-3) / 1e9, "ms": ms, "n_unique": nu,
             "gpu_launches": 8}

@@ -81,6 +81,7 @@ class Port:
         lib.wo_pairwise_sum.argtypes = [vp, u64]
         lib.wo_weights_check.argtypes = [vp, u64, vp, vp, vp, vp]
         lib.wo_generate_uniform.argtypes = [u64, u64, vp]
+        lib.wo_generate_lognormal.argtypes = [u64, f64, u64, vp]
         lib.wo_generate_powerlaw.argtypes = [u64, f64, u64, vp]
         lib.wo_prefix_sums.argtypes = [vp, vp, u64]
         lib.wo_scan_block_totals.argtypes = [vp, u64, vp]
@@ -105,6 +106,12 @@ class Port:
     def generate_uniform(self, n: int, seed: int) -> np.ndarray:
         out = np.empty(n, np.float64)
         self.lib.wo_generate_uniform(n, seed, _ptr(out))
+        return out
+
+    def generate_lognormal(self, n: int, sigma: float, seed: int) -> np.ndarray:
+        """configs[3]'s weights (the library's own generator, restated)."""
+        out = np.empty(n, np.float64)
+        self.lib.wo_generate_lognormal(n, C.c_double(sigma), seed, _ptr(out))
         return out
 
     def generate_powerlaw(self, n: int, s: float, seed: int) -> np.ndarray:

@@ -93,6 +93,89 @@ int wo_generate_powerlaw(uint64_t n, double s, uint64_t seed, double* out) {
     return 0;
 }
 
+/* generate_lognormal: configs[3]'s weights -- NOT a reference generator (the
+ * reference has none); the library's own, defined in
+ * paper_1903_00227_b200/csrc/common.cuh (lognormal_weight) and restated
+ * here operation for operation so the reference can be fed the same bytes:
+ * item i takes outputs 2i+1, 2i+2 of RngStream(seed, 'logn'),
+ * w = exp(sigma * sqrt(-2 log(1 - u1)) * cos(2 pi u2)), with log / cos / exp
+ * evaluated by the same argument reductions and Horner series. */
+static const double kLn2Hi = 0x1.62e42fefa3800p-1, kLn2Lo = 0x1.ef35793c76730p-45;
+
+static double det_log(double x) {
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    int e = (int)((b >> 52) & 0x7ff) - 1023;
+    b = (b & UINT64_C(0x000fffffffffffff)) | UINT64_C(0x3ff0000000000000);
+    double m;
+    memcpy(&m, &b, 8);
+    if (m > 1.4142135623730951) {
+        m = m * 0.5;
+        e += 1;
+    }
+    const double s = (m - 1.0) / (m + 1.0), s2 = s * s;
+    static const double c[13] = {1.0 / 25.0, 1.0 / 23.0, 1.0 / 21.0, 1.0 / 19.0, 1.0 / 17.0,
+                                 1.0 / 15.0, 1.0 / 13.0, 1.0 / 11.0, 1.0 / 9.0,  1.0 / 7.0,
+                                 1.0 / 5.0,  1.0 / 3.0,  1.0};
+    double p = c[0];
+    for (int k = 1; k < 13; ++k) p = p * s2 + c[k];
+    const double de = (double)e;
+    return de * kLn2Hi + (de * kLn2Lo + 2.0 * s * p);
+}
+
+static double det_cos2pi(double u) {
+    double a = u - 0.5;
+    a = a < 0.0 ? -a : a;
+    double sign = -1.0;
+    if (a > 0.25) {
+        a = 0.5 - a;
+        sign = 1.0;
+    }
+    const double t = a * 6.283185307179586, t2 = t * t;
+    static const double c[13] = {1.0 / 620448401733239439360000.0, 1.0 / 1124000727777607680000.0,
+                                 1.0 / 2432902008176640000.0,      1.0 / 6402373705728000.0,
+                                 1.0 / 20922789888000.0,           1.0 / 87178291200.0,
+                                 1.0 / 479001600.0,                1.0 / 3628800.0,
+                                 1.0 / 40320.0,                    1.0 / 720.0,
+                                 1.0 / 24.0,                       1.0 / 2.0,
+                                 1.0};
+    double p = c[0];
+    for (int k = 1; k < 13; ++k) p = p * -t2 + c[k];
+    return sign * p;
+}
+
+static double det_exp(double x) {
+    const double kf = floor(x * 1.4426950408889634 + 0.5);
+    const double r = (x - kf * kLn2Hi) - kf * kLn2Lo;
+    static const double c[19] = {1.0 / 355687428096000.0, 1.0 / 20922789888000.0,
+                                 1.0 / 1307674368000.0,   1.0 / 87178291200.0,
+                                 1.0 / 6227020800.0,      1.0 / 479001600.0,
+                                 1.0 / 39916800.0,        1.0 / 3628800.0,
+                                 1.0 / 362880.0,          1.0 / 40320.0,
+                                 1.0 / 5040.0,            1.0 / 720.0,
+                                 1.0 / 120.0,             1.0 / 24.0,
+                                 1.0 / 6.0,               0.5,
+                                 1.0,                     1.0};
+    double p = c[0];
+    for (int k = 1; k < 18; ++k) p = p * r + c[k];
+    const uint64_t eb = (uint64_t)((int64_t)kf + 1023) << 52;
+    double scale;
+    memcpy(&scale, &eb, 8);
+    return p * scale;
+}
+
+void wo_generate_lognormal(uint64_t n, double sigma, uint64_t seed, double* out) {
+    const wo_rng rng = wo_rng_make(seed, 0x6c6f676eu); /* 'logn' */
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t r1 = wo_mix64(rng.key + (2 * i + 1) * kGolden);
+        const uint64_t r2 = wo_mix64(rng.key + (2 * i + 2) * kGolden);
+        const double u1 = 1.0 - (double)(r1 >> 11) * 0x1.0p-53;
+        const double u2 = (double)(r2 >> 11) * 0x1.0p-53;
+        const double z = sqrt(-2.0 * det_log(u1)) * det_cos2pi(u2);
+        out[i] = det_exp(sigma * z);
+    }
+}
+
 /* ------------------------------------------------------------ weights */
 
 /* pairwise_sum: weights.hpp:19-28 -- leaves of <= 32 summed left to right,

@@ -48,6 +48,9 @@ void wo_rng_outputs(uint64_t seed, uint64_t stream, int64_t salt, uint64_t count
 /* Weight generators (weight_file.hpp:32-54). Return 0 on success. */
 void wo_generate_uniform(uint64_t n, uint64_t seed, double* out);
 int wo_generate_powerlaw(uint64_t n, double s, uint64_t seed, double* out);
+/* configs[3]'s lognormal(0, sigma) weights: the library's own generator
+ * (common.cuh lognormal_weight), restated. */
+void wo_generate_lognormal(uint64_t n, double sigma, uint64_t seed, double* out);
 
 /* WeightTable (weights.hpp:19-46): returns 0 if valid, else 1 and *bad =
  * first offending index.  *total = pairwise_sum. */

@@ -243,6 +243,25 @@ bool psa_exact_env() {
     return e && e[0] == '1';
 }
 
+// configs[3]'s lognormal(0, sigma) weights, items [offset, offset + n) of the
+// global vector (counter-based: only the slice is generated).
+std::shared_ptr<WeightsData> lognormal_device(uint64_t n, uint64_t offset, double sigma,
+                                              uint64_t seed) {
+    if (!(sigma >= 0.0) || !std::isfinite(sigma) || sigma > 30.0)
+        throw std::invalid_argument("lognormal sigma must be in [0, 30]");
+    if (n == 0) throw std::invalid_argument("weights: need at least one item");
+    auto wd = std::make_shared<WeightsData>();
+    wd->device = current_device();
+    wd->n = n;
+    wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
+    wd->d_w = static_cast<double*>(wd->storage->p);
+    Stream st;
+    ck(wrsb::launch_generate_lognormal(wd->d_w, n, offset, seed, sigma, st.s), "generate");
+    ck(cudaStreamSynchronize(st.s), "generate");
+    finalize_weights(*wd, "");
+    return wd;
+}
+
 }  // namespace
 
 struct wrs_weights {
@@ -561,6 +580,10 @@ wrs_status wrs_weights_generate(const char* dist, double param, uint64_t n, uint
             *out = new wrs_weights{powerlaw_device(n, param, seed)};
             return WRS_OK;
         }
+        if (d == "lognormal") {
+            *out = new wrs_weights{lognormal_device(n, 0, param, seed)};
+            return WRS_OK;
+        }
         return fail(WRS_EINVAL, "unknown distribution: " + d);
     });
 }
@@ -752,9 +775,13 @@ wrs_status wrs_b200_weights_generate_range(const char* dist, double param, uint6
     if (!dist || !out) return fail(WRS_EINVAL, "null argument");
     return guarded([&]() -> wrs_status {
         const std::string d = dist;
-        if (d != "uniform" && d != "powerlaw")
+        if (d != "uniform" && d != "powerlaw" && d != "lognormal")
             return fail(WRS_EINVAL, "unknown distribution: " + d);
         if (lo >= hi || hi > n_total) return fail(WRS_EINVAL, "bad range");
+        if (d == "lognormal") {
+            *out = new wrs_weights{lognormal_device(hi - lo, lo, param, seed)};
+            return WRS_OK;
+        }
         if (d == "powerlaw") {
             // the deal is global: generate all n_total, keep [lo, hi)
             auto full = powerlaw_device(n_total, param, seed);

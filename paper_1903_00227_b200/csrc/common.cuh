@@ -6,7 +6,9 @@
 // (the reference's x86-64 build has no FMA).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace wrsb {
@@ -72,6 +74,117 @@ __host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k
         k0 += W0;
         k1 += W1;
     }
+}
+
+// ---- configs[3]'s lognormal weights (our own generator) ------
+// The reference has no lognormal generator, so this one is defined here and
+// restated in the oracle (oracle/wrs_oracle.c, wo_generate_lognormal): item
+// i of generate_lognormal(n, sigma, seed) takes outputs 2i+1 and 2i+2 of
+// RngStream(seed, 'logn'):
+//     u1 = 1 - uniform01()  in (0, 1],  u2 = uniform01()  in [0, 1)
+//     z  = sqrt(-2 log u1) cos(2 pi u2)          (Box-Muller, one variate)
+//     w  = exp(sigma z)                          (lognormal(0, sigma))
+// log, cos and exp are evaluated by the fixed sequences of IEEE additions,
+// multiplications and divisions below (argument reduction + Horner series,
+// no fused multiply-adds), so the CPU and the GPU produce the same bits.
+constexpr uint64_t kLognStream = 0x6c6f676eu;  // "logn"
+constexpr double kLn2Hi = 0x1.62e42fefa3800p-1, kLn2Lo = 0x1.ef35793c76730p-45;
+
+// log x for x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt(2)); log m =
+// 2 atanh(s), s = (m - 1) / (m + 1), |s| < 0.172: 13 odd terms.
+__host__ __device__ inline double det_log(double x) {
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    int e = static_cast<int>((b >> 52) & 0x7ff) - 1023;
+    b = (b & 0x000fffffffffffffull) | 0x3ff0000000000000ull;
+    double m;
+    memcpy(&m, &b, 8);
+    if (m > 1.4142135623730951) {
+        m = m * 0.5;
+        e += 1;
+    }
+    const double s = (m - 1.0) / (m + 1.0);
+    const double s2 = s * s;
+    double p = 1.0 / 25.0;
+    p = p * s2 + 1.0 / 23.0;
+    p = p * s2 + 1.0 / 21.0;
+    p = p * s2 + 1.0 / 19.0;
+    p = p * s2 + 1.0 / 17.0;
+    p = p * s2 + 1.0 / 15.0;
+    p = p * s2 + 1.0 / 13.0;
+    p = p * s2 + 1.0 / 11.0;
+    p = p * s2 + 1.0 / 9.0;
+    p = p * s2 + 1.0 / 7.0;
+    p = p * s2 + 1.0 / 5.0;
+    p = p * s2 + 1.0 / 3.0;
+    p = p * s2 + 1.0;
+    const double de = static_cast<double>(e);
+    return de * kLn2Hi + (de * kLn2Lo + 2.0 * s * p);
+}
+// cos(2 pi u) for u in [0, 1): cos(2 pi u) = -cos(2 pi (u - 1/2)), folded to
+// an angle in [0, pi/2]; even Taylor series, 13 terms.
+__host__ __device__ inline double det_cos2pi(double u) {
+    double a = u - 0.5;
+    a = a < 0.0 ? -a : a;
+    double sign = -1.0;
+    if (a > 0.25) {
+        a = 0.5 - a;
+        sign = 1.0;
+    }
+    const double t = a * 6.283185307179586;
+    const double t2 = t * t;
+    double p = 1.0 / 620448401733239439360000.0;   // 1/24!
+    p = p * -t2 + 1.0 / 1124000727777607680000.0;  // 1/22!
+    p = p * -t2 + 1.0 / 2432902008176640000.0;     // 1/20!
+    p = p * -t2 + 1.0 / 6402373705728000.0;        // 1/18!
+    p = p * -t2 + 1.0 / 20922789888000.0;          // 1/16!
+    p = p * -t2 + 1.0 / 87178291200.0;             // 1/14!
+    p = p * -t2 + 1.0 / 479001600.0;               // 1/12!
+    p = p * -t2 + 1.0 / 3628800.0;                 // 1/10!
+    p = p * -t2 + 1.0 / 40320.0;                   // 1/8!
+    p = p * -t2 + 1.0 / 720.0;                     // 1/6!
+    p = p * -t2 + 1.0 / 24.0;                      // 1/4!
+    p = p * -t2 + 1.0 / 2.0;                       // 1/2!
+    p = p * -t2 + 1.0;
+    return sign * p;
+}
+// exp x for |x| < 700: x = k ln2 + r, |r| <= ln2 / 2; Taylor series of e^r
+// (18 terms) times 2^k.
+__host__ __device__ inline double det_exp(double x) {
+    const double kf = floor(x * 1.4426950408889634 + 0.5);
+    const double r = (x - kf * kLn2Hi) - kf * kLn2Lo;
+    double p = 1.0 / 355687428096000.0;  // 1/17!
+    p = p * r + 1.0 / 20922789888000.0;  // 1/16!
+    p = p * r + 1.0 / 1307674368000.0;   // 1/15!
+    p = p * r + 1.0 / 87178291200.0;     // 1/14!
+    p = p * r + 1.0 / 6227020800.0;      // 1/13!
+    p = p * r + 1.0 / 479001600.0;       // 1/12!
+    p = p * r + 1.0 / 39916800.0;        // 1/11!
+    p = p * r + 1.0 / 3628800.0;         // 1/10!
+    p = p * r + 1.0 / 362880.0;          // 1/9!
+    p = p * r + 1.0 / 40320.0;           // 1/8!
+    p = p * r + 1.0 / 5040.0;            // 1/7!
+    p = p * r + 1.0 / 720.0;             // 1/6!
+    p = p * r + 1.0 / 120.0;             // 1/5!
+    p = p * r + 1.0 / 24.0;              // 1/4!
+    p = p * r + 1.0 / 6.0;               // 1/3!
+    p = p * r + 0.5;                     // 1/2!
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    const uint64_t eb = static_cast<uint64_t>(static_cast<int64_t>(kf) + 1023) << 52;
+    double scale;
+    memcpy(&scale, &eb, 8);
+    return p * scale;
+}
+// weight of item g (a global index) of generate_lognormal(., sigma, seed),
+// key = rng_key(seed, kLognStream)
+__host__ __device__ inline double lognormal_weight(uint64_t key, uint64_t g, double sigma) {
+    const uint64_t r1 = mix64(key + (2 * g + 1) * kGolden);
+    const uint64_t r2 = mix64(key + (2 * g + 2) * kGolden);
+    const double u1 = 1.0 - static_cast<double>(r1 >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(r2 >> 11) * 0x1.0p-53;
+    const double z = sqrt(-2.0 * det_log(u1)) * det_cos2pi(u2);
+    return det_exp(sigma * z);
 }
 
 #if defined(__CUDACC__)

@@ -166,5 +166,9 @@ cudaError_t fisher_yates_device(const double* d_in, double* d_out, uint64_t n, u
 // the global vector (a shard's slice).
 cudaError_t launch_generate_uniform(double* d_w, uint64_t n, uint64_t offset, uint64_t seed,
                                     cudaStream_t st);
+// configs[3]'s lognormal(0, sigma) weights (common.cuh: lognormal_weight),
+// items [offset, offset + n) of the global vector.
+cudaError_t launch_generate_lognormal(double* d_w, uint64_t n, uint64_t offset, uint64_t seed,
+                                      double sigma, cudaStream_t st);
 
 }  // namespace wrsb

@@ -919,6 +919,14 @@ __global__ void k_generate_uniform(double* __restrict__ w, uint64_t n, uint64_t 
     }
 }
 
+__global__ void k_generate_lognormal(double* __restrict__ w, uint64_t n, uint64_t offset,
+                                     uint64_t key, double sigma) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += stride)
+        w[i] = lognormal_weight(key, offset + i, sigma);  // common.cuh
+}
+
 static int sm_count() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1317,6 +1325,17 @@ cudaError_t launch_generate_uniform(double* d_w, uint64_t n, uint64_t offset, ui
     if (blocks > cap) blocks = cap;
     k_generate_uniform<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         d_w, n, offset, rng_key(seed, 0x67656e75u));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate_lognormal(double* d_w, uint64_t n, uint64_t offset, uint64_t seed,
+                                      double sigma, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
+    if (blocks > cap) blocks = cap;
+    k_generate_lognormal<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        d_w, n, offset, rng_key(seed, kLognStream), sigma);
     return cudaGetLastError();
 }
 

@@ -123,9 +123,8 @@ def test_counts_full_size_lognormal_chi_square():
     reference's chi-square policy against w_i / W."""
     import torch
     n, k = 10**8, 10**9
-    g = torch.Generator(device="cuda").manual_seed(42)
-    wt = torch.exp(2.0 * torch.randn(n, dtype=torch.float64, device="cuda", generator=g))
-    W = wrs.Weights.from_device(wt)
+    W = wrs.Weights.generate("lognormal", 2.0, n, 42)  # configs[3]'s generator
+    wt = torch.from_numpy(W.values()).cuda()
     S = wrs.Sampler.build(W, "psa", 1)
     d_items = torch.empty(n, dtype=torch.int32, device="cuda")
     d_counts = torch.empty(n, dtype=torch.int64, device="cuda")

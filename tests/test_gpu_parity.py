@@ -515,3 +515,15 @@ def test_region_plan_slab_redirect_and_overflow(P, ov_cap, monkeypatch):
         items, counts = S.draw_counts(31, k, Wk)
         ri, rc = np.unique(ref, return_counts=True)
         assert np.array_equal(items, ri) and np.array_equal(counts, rc), Wk
+
+
+def test_lognormal_device_generator_matches_oracle(P):
+    """configs[3]'s weights: wrs_weights_generate("lognormal", sigma, ...) on
+    the device equals the oracle's restatement byte for byte (whole vector and
+    a shard's slice), so the CPU reference can be fed the same input."""
+    n = 1_000_003
+    ref = P.generate_lognormal(n, 2.0, 42)
+    W = wrs.Weights.generate("lognormal", 2.0, n, 42)
+    assert W.values().tobytes() == ref.tobytes()
+    S = wrs.Weights.generate_range("lognormal", 2.0, n, 123_457, 654_321, 42)
+    assert S.values().tobytes() == ref[123_457:654_321].tobytes()

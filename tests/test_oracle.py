@@ -212,3 +212,20 @@ def test_philox_known_answers(P):
             (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1))]
     for ctr, key, want in kat:
         assert tuple(int(x) for x in P.philox4x32_10(ctr, key)) == want
+
+
+def test_lognormal_generator_is_accurate_box_muller():
+    """configs[3]'s own generator (common.cuh lognormal_weight, restated in
+    the oracle): its fixed-sequence log / cos / exp agree with libm to a few
+    ulps, on the same RngStream(seed, 'logn') outputs (2i+1, 2i+2)."""
+    P = oracle.port()
+    n, sigma, seed = 20000, 2.0, 42
+    w = P.generate_lognormal(n, sigma, seed)
+    r = P.rng_outputs(seed, 0x6C6F676E, -1, 2 * n).reshape(n, 2)
+    u1 = 1.0 - (r[:, 0] >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    u2 = (r[:, 1] >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2 * np.pi * u2)
+    ref = np.exp(sigma * z)
+    assert np.max(np.abs(w - ref) / ref) < 1e-12
+    assert abs(np.log(w).mean()) < 0.05 and abs(np.log(w).std() - sigma) < 0.05
+    assert np.all(w > 0) and np.all(np.isfinite(w))
