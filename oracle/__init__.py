@@ -301,6 +301,7 @@ class Ref:
         lib.ref_table_free.argtypes = [vp]
         lib.ref_table_buckets.argtypes = [vp, vp, C.POINTER(f64)]
         lib.ref_table_sample_many.argtypes = [vp, u64, u64, C.c_uint, vp]
+        lib.ref_build_method.argtypes = [vp, u64, C.c_int, vp, C.POINTER(f64)]
         lib.ref_wt_new.restype = vp
         lib.ref_wt_new.argtypes = [vp, u64]
         lib.ref_wt_free.argtypes = [vp]
@@ -366,6 +367,16 @@ class Ref:
         out = np.zeros(w.size, BUCKET_DTYPE)
         wn = f64()
         if self.lib.ref_psa_build(_ptr(w), w.size, workers, _ptr(out), C.byref(wn)):
+            raise ValueError("reference build failed")
+        return out, wn.value
+
+    def build_method(self, w, method: str):
+        """AliasTable(wt, Build::vose | Build::sweep) of the reference."""
+        w = np.ascontiguousarray(w, np.float64)
+        out = np.zeros(w.size, BUCKET_DTYPE)
+        wn = f64()
+        if self.lib.ref_build_method(_ptr(w), w.size, {"vose": 0, "sweep": 1}[method], _ptr(out),
+                                     C.byref(wn)):
             raise ValueError("reference build failed")
         return out, wn.value
 

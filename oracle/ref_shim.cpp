@@ -179,6 +179,21 @@ int ref_psa_plan(const double* w, uint64_t n, uint64_t P, uint64_t* bounds, doub
     }
 }
 
+/* AliasTable(wt, Build::vose / Build::sweep) -- the reference's other
+ * builders (alias.hpp:299-409), extra oracles for the masses.
+ * method: 0 = vose, 1 = sweep.  Returns 0 on success. */
+int ref_build_method(const double* w, uint64_t n, int method, void* buckets, double* bucket_mean) {
+    try {
+        auto wt = table_of(w, n);
+        wrs::AliasTable t(wt, method == 0 ? wrs::AliasTable::Build::vose : wrs::AliasTable::Build::sweep);
+        copy_buckets(t.buckets(), buckets);
+        *bucket_mean = t.bucket_mean();
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
 /* A reference table kept alive for sampling / verification. */
 void* ref_table_new(const double* w, uint64_t n, unsigned workers) {
     try {

@@ -167,3 +167,26 @@ def test_multi_calls_validate_arguments():
     assert L.wrs_b200_multi_counts(None, 1, 1, None) == wrs.wrs.WRS_EINVAL
     assert L.wrs_b200_multi_shard(None) is None
     L.wrs_b200_multi_free(None)
+
+
+def build_capi_client(tmp_dir) -> str:
+    """Compile tests/capi_client.c (plain C, include/wrs.h) and link it to
+    libwrs_b200.so the way a reference client links libwrs."""
+    import subprocess
+    exe = os.path.join(str(tmp_dir), "capi_client")
+    libdir = os.path.dirname(wrs.wrs.LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "capi_client.c"), "-o", exe, "-L", libdir,
+                    "-l:libwrs_b200.so", f"-Wl,-rpath,{libdir}"], check=True)
+    return exe
+
+
+def test_c_client_links_and_fails_loudly_without_gpu(tmp_path):
+    import subprocess
+    from tests.conftest import cuda_available
+    if cuda_available():
+        pytest.skip("GPU present: test_gpu_parity runs the client for real")
+    exe = build_capi_client(tmp_path)
+    r = subprocess.run([exe, "--no-gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "capi client ok" in r.stdout

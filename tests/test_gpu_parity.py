@@ -527,3 +527,38 @@ def test_lognormal_device_generator_matches_oracle(P):
     assert W.values().tobytes() == ref.tobytes()
     S = wrs.Weights.generate_range("lognormal", 2.0, n, 123_457, 654_321, 42)
     assert S.values().tobytes() == ref[123_457:654_321].tobytes()
+
+
+def test_c_client_through_the_reference_abi(tmp_path):
+    """tests/capi_client.c: a plain C program against include/wrs.h, linked
+    to libwrs_b200.so (the reference client flow, test_capi.cpp:12-112)."""
+    import subprocess
+    from tests.test_capi_host import build_capi_client
+    exe = build_capi_client(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr
+    assert "capi client ok" in r.stdout
+
+
+def test_masses_agree_with_reference_vose_and_sweep(P):
+    """the reference's other builders as extra oracles.  The
+    GPU PSA table, the reference's Build::vose and Build::sweep tables
+    (alias.hpp:299-409, run through oracle/_ref) are different tables whose
+    implied masses (verify.hpp:43-54) must all reproduce w_i within the
+    reference's own tolerance, and agree with each other."""
+    R = oracle.ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    cases = [P.generate_uniform(200_003, 1), P.generate_powerlaw(100_000, 1.0, 2),
+             np.exp(rng.normal(0.0, 2.0, 50_000)), np.concatenate([[1e6], np.ones(9999)])]
+    for w in cases:
+        W = wrs.Weights.from_array(w)
+        S = wrs.Sampler.build(W, "psa", 1)
+        gm, worst = S.implied_masses()
+        assert worst < 1e-9
+        for method in ("vose", "sweep"):
+            b, wn = R.build_method(w, method)
+            rm = R.implied_masses(b, wn)
+            assert np.max(np.abs(rm - w) / w) < 1e-9, method
+            assert np.max(np.abs(rm - gm) / w) < 2e-9, method
