@@ -28,6 +28,12 @@ WRS_API uint64_t wrs_b200_default_jobs(uint64_t n);
  * and the number of bytes released. */
 WRS_API uint64_t wrs_b200_release_cache(void);
 
+/* Checked builds (make -C paper_1903_00227_b200/csrc checked ->
+ * libwrs_b200_checked.so): the number of device-side index-check violations
+ * so far, the first offending source line in *first_line.  -1 in the normal
+ * build (no checks compiled in). */
+WRS_API int64_t wrs_b200_check_failures(unsigned* first_line);
+
 /* Weights already in device memory of the current CUDA device.  copy != 0
  * duplicates them; copy == 0 borrows d_w (caller keeps it alive and
  * unchanged until every handle built from it is freed). */

@@ -6,14 +6,15 @@ The product is libwrs_b200.so (csrc/); this package only binds it.
 import os
 import subprocess
 
-from .wrs import (BUCKET_DTYPE, MultiSampler, Sampler, Weights, WrsError, default_jobs,
+from .wrs import (BUCKET_DTYPE, MultiSampler, Sampler, Weights, WrsError, check_failures,
+                  default_jobs,
                   last_error, lib, nccl_available, nccl_unique_id, release_cache,
                   sample_with_replacement, set_timing, shard_counts, shard_range, shard_seed,
                   status_name)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-__all__ = ["BUCKET_DTYPE", "MultiSampler", "Sampler", "Weights", "WrsError", "build",
+__all__ = ["BUCKET_DTYPE", "MultiSampler", "Sampler", "Weights", "WrsError", "build", "check_failures",
            "default_jobs", "last_error", "lib", "nccl_available", "nccl_unique_id",
            "release_cache", "sample_with_replacement", "set_timing", "shard_counts",
            "shard_range", "shard_seed", "status_name"]

@@ -747,6 +747,18 @@ uint64_t wrs_b200_default_jobs(uint64_t n) { return wrsb::default_jobs(n); }
 
 uint64_t wrs_b200_release_cache(void) { return wrsb::release_cache(); }
 
+int64_t wrs_b200_check_failures(unsigned* first_line) {
+#ifdef WRS_B200_CHECKED
+    if (first_line) *first_line = 0;
+    return static_cast<int64_t>(
+        wrsb::check_failures_psa(first_line) + wrsb::check_failures_sample(first_line) +
+        wrsb::check_failures_verify(first_line) + wrsb::check_failures_generate(first_line));
+#else
+    if (first_line) *first_line = 0;
+    return -1;
+#endif
+}
+
 wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
                                         wrs_weights** out) {
     if (!d_w || !out) return fail(WRS_EINVAL, "null argument");

@@ -188,6 +188,41 @@ __host__ __device__ inline double lognormal_weight(uint64_t key, uint64_t g, dou
 }
 
 #if defined(__CUDACC__)
+// ---- checked builds (make checked -> libwrs_b200_checked.so) ---------------
+// compute-sanitizer is not available on the GPU pool, so the library checks
+// itself: in a checked build every WRS_CHECK'd index is tested on the device
+// and a violation is counted (the first offending source line is kept) in a
+// per-translation-unit counter that wrs_b200_check_failures() reads; scratch
+// buffers are also filled with 0xFF bytes (NaN / huge indices) before use, so
+// a read of anything not written first shows up in the parity checks.  In
+// the normal build WRS_CHECK compiles to nothing.
+#ifdef WRS_B200_CHECKED
+static __device__ unsigned long long g_check_fail = 0;
+static __device__ unsigned int g_check_line = 0;
+__device__ __noinline__ static void check_fail(unsigned line) {
+    atomicAdd(&g_check_fail, 1ull);
+    atomicCAS(&g_check_line, 0u, line);
+}
+#define WRS_CHECK(c)                                 \
+    do {                                             \
+        if (!(c)) ::wrsb::check_fail(__LINE__);      \
+    } while (0)
+// this translation unit's count (and first line); host side
+static inline unsigned long long tu_check_failures(unsigned* line) {
+    unsigned long long c = 0;
+    unsigned l = 0;
+    cudaMemcpyFromSymbol(&c, g_check_fail, sizeof c);
+    cudaMemcpyFromSymbol(&l, g_check_line, sizeof l);
+    if (line && l && !*line) *line = l;
+    return c;
+}
+#else
+#define WRS_CHECK(c) \
+    do {             \
+    } while (0)
+static inline unsigned long long tu_check_failures(unsigned*) { return 0; }
+#endif
+
 // Neumaier compensated sum, parallel.hpp:70-81 (the isfinite guard keeps an
 // infinite running value from poisoning the low word).  Written branch-free:
 // the error term is always computed and the guarded update is a select, so

@@ -10,6 +10,15 @@
 
 namespace wrsb {
 
+// Checked builds: device-side index violations counted per translation unit
+// (common.cuh WRS_CHECK); *line gets the first offending source line.
+unsigned long long check_failures_psa(unsigned* line);
+unsigned long long check_failures_sample(unsigned* line);
+unsigned long long check_failures_verify(unsigned* line);
+unsigned long long check_failures_generate(unsigned* line);
+// Checked builds fill scratch with 0xFF bytes (no-op otherwise).
+void poison(void* p, size_t bytes, cudaStream_t st);
+
 // Caching device allocator for the library's large buffers (alloc.cpp).
 cudaError_t dev_malloc(void** p, size_t bytes);
 void dev_free(void* p);

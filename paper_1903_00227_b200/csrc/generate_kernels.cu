@@ -178,4 +178,6 @@ cudaError_t fisher_yates_device(const double* d_in, double* d_out, uint64_t n, u
     return e;
 }
 
+unsigned long long check_failures_generate(unsigned* line) { return tu_check_failures(line); }
+
 }  // namespace wrsb

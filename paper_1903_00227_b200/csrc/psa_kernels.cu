@@ -347,6 +347,7 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
     }
     __syncthreads();
     const uint64_t L0 = s_excl, H0 = base - s_excl;
+    WRS_CHECK(L0 + totL <= n && H0 + totH <= n);
     for (uint32_t p = tid; p < totL; p += K1_THREADS) lw[L0 + p] = sw[p];
     for (uint32_t p = tid; p < totH; p += K1_THREADS) {
         hidx[H0 + p] = static_cast<uint32_t>(base + sidx[totL + p]);
@@ -416,6 +417,7 @@ k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, De
     __syncthreads();
     const uint64_t L0 = s_excl, H0 = base - s_excl;
     const unsigned lt = lanemask_lt();
+    WRS_CHECK(tile < ntiles && L0 + C.totL <= n && H0 + C.totH <= n);
 #pragma unroll
     for (int r = 0; r < K1_ROWS; ++r) {
         const int cell = r * K1_WARPS + warp;
@@ -627,6 +629,7 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
                 }
             }
             double2* d = ck + 2 * c;
+            WRS_CHECK(static_cast<uint64_t>(c) * K2_C < static_cast<uint64_t>(me.len));
             __stcs(d, k0);
             __stcs(d + 1, k1);
         }
@@ -1166,6 +1169,7 @@ struct CkList {
     uint64_t len;
 };
 __device__ __forceinline__ double ck_value(const CkList& L, uint64_t m) {
+    WRS_CHECK(m * CK_STRIDE < L.len);
     const double2 s = __ldg(L.ck + m);
     return s.x + s.y;
 }
@@ -1175,6 +1179,7 @@ __device__ __forceinline__ double ck_exact(const CkList& L, uint64_t x) {
     const uint64_t e = x - 1;
     const double2 s = __ldg(L.ck + (e / CK_STRIDE));
     CompSumPos cs{s.x, s.y};
+    WRS_CHECK(e < L.len);
     for (uint64_t p = e & ~static_cast<uint64_t>(CK_STRIDE - 1); p <= e; ++p) cs.add(__ldg(L.w + p));
     return cs.value();
 }
@@ -1306,7 +1311,7 @@ __device__ __forceinline__ void cp_async16_ordered(void* smem, const void* gmem)
 template <int PASSES>
 __device__ __forceinline__ void k4_rows(K4Rings& R, const double* __restrict__ lw,
                                         const double* __restrict__ hw, uint32_t* __restrict__ lrank,
-                                        double* __restrict__ hshare) {
+                                        double* __restrict__ hshare, uint64_t nl, uint64_t nh) {
     const int lane = threadIdx.x & 31;
     const uint32_t q2 = 2u * (lane & 7);
     const int quarter = lane >> 3;
@@ -1317,6 +1322,10 @@ __device__ __forceinline__ void k4_rows(K4Rings& R, const double* __restrict__ l
         const uint32_t c = R.cnt[r];
         const uint32_t fle = d.x + (c & 0xffu), fhe = d.y + ((c >> 8) & 0xffu);
         const uint32_t rle = d.z + ((c >> 16) & 0xffu), rhe = d.w + (c >> 24);
+        // flushes stay inside the lists; refills may read one pair element
+        // past a list end (the buffers' slack)
+        WRS_CHECK(fle <= nl && fhe <= nh && rle <= nl + 2 && rhe <= nh + 2);
+        (void)nl, (void)nh;
         double* const Lr = R.l[r];
         double* const Hr = R.h[r];
 #pragma unroll
@@ -1429,7 +1438,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* 
         __syncwarp();
     };
     post();
-    k4_rows<2>(R, lw, hw, lrank, hshare);  // prologue: two phases' worth of inputs
+    k4_rows<2>(R, lw, hw, lrank, hshare, sc->nl, nh64);  // prologue: two phases' worth of inputs
     cp_async_commit();
     cp_async_commit();  // (empty: phase 0 waits for the prologue alone)
 
@@ -1506,7 +1515,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* 
         __syncwarp();
         // this phase's outputs out, the phase after next's inputs in
         post();
-        k4_rows<1>(R, lw, hw, lrank, hshare);
+        k4_rows<1>(R, lw, hw, lrank, hshare, sc->nl, nh64);
         cp_async_commit();
     }
     cp_async_wait<0>();
@@ -1607,6 +1616,7 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
             rank = min(static_cast<uint32_t>(H0) + q + 1, hmax);  // heavy_at(j + 1)
         }
         const uint32_t o = rank - wlo32;
+        WRS_CHECK(rank < nh);
         const uint32_t id = (ids && o < wn32) ? d_id[o] : __ldg(hidx + rank);
         store_bucket(out, gi, share, static_cast<uint32_t>(gi), id);
     }
@@ -1792,6 +1802,20 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(ws.tile_status, 0, ntiles * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
+    // checked builds: every scratch array starts as 0xFF garbage
+    poison(ws.lw, ws.n * 8, st);
+    poison(ws.hw, ws.n * 8, st);
+    poison(ws.hidx, ws.n * 4, st);
+    poison(ws.lpre, (ws.n + 1) * 8, st);
+    poison(ws.hpre, (ws.n + 1) * 8, st);
+    poison(ws.lck, (ws.n / CK_STRIDE + 2) * 16, st);
+    poison(ws.hck, (ws.n / CK_STRIDE + 2) * 16, st);
+    poison(ws.totals, (ws.n / SCAN_BLOCK + 3) * 8, st);
+    poison(ws.carries, (ws.n / SCAN_BLOCK + 3) * 8, st);
+    poison(ws.split_l, (P + 1) * 4, st);
+    poison(ws.split_h, (P + 1) * 4, st);
+    poison(ws.split_s, (P + 1) * 8, st);
+    poison(d_b, n * sizeof(Bucket), st);
     REC(0);
     if (k1_staged())
         k_partition<<<static_cast<unsigned>(ntiles), K1_THREADS, k1_smem, st>>>(
@@ -1862,6 +1886,16 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     REC(7);
 #undef REC
     return cudaGetLastError();
+}
+
+unsigned long long check_failures_psa(unsigned* line) { return tu_check_failures(line); }
+
+void poison(void* p, size_t bytes, cudaStream_t st) {
+#ifdef WRS_B200_CHECKED
+    if (p && bytes) cudaMemsetAsync(p, 0xff, bytes, st);
+#else
+    (void)p, (void)bytes, (void)st;
+#endif
 }
 
 }  // namespace wrsb

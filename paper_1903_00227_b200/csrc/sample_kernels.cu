@@ -243,6 +243,7 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
 #pragma unroll
         for (int u = 0; u < K5_UNROLL; ++u) {
             const uint64_t q = q0 + static_cast<uint64_t>(u) * K5_THREADS;
+            WRS_CHECK(q >= q_end || bidx[u] < g.n);
             if (q < q_end) out[q] = pick(bk[u], x[u]) + out_base;
         }
     }
@@ -477,6 +478,8 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         const uint32_t i = r * TT + threadIdx.x;
         if (i < kc_left) {
             const uint2 v = stage[i];
+            WRS_CHECK(v.y < n32 && goff[v.y >> rg.shift] + i <
+                                          static_cast<uint64_t>(rg.nreg) * rg.cap + rg.ov_cap);
             uint2* dst = rec + (goff[v.y >> rg.shift] + i);
             asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
                          :: "l"(dst), "r"(v.x), "r"(v.y), "l"(pol));
@@ -520,6 +523,9 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
     }
+#pragma unroll
+    for (int u = 0; u < RC_ROWS; ++u)
+        WRS_CHECK(p0 + u * 256 + threadIdx.x >= valid_end || r[u].y < rg.g.n);
     // bucket gathers as LDGSTS into shared memory: measured 232 G random
     // L2-resident 16-B rows/s vs 200 G for LDG (scripts/microbench/
     // l2_gather_bench.cu); each thread reads back only its own rows
@@ -635,8 +641,10 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
             *reinterpret_cast<uint4*>(out + tbase + e0) = o;
         }
     } else {
-        for (uint32_t e = threadIdx.x; e < tcount; e += TT)
+        for (uint32_t e = threadIdx.x; e < tcount; e += TT) {
+            WRS_CHECK(slot_of[tbase + e] < tcount);
             out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
+        }
     }
 }
 
@@ -653,6 +661,7 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
 // ===========================================================================
 // hits[0, n): draws answered by bucket b itself; hits[n, 2n): by its alias
 __device__ __forceinline__ void count_hit(uint32_t* hits, uint64_t n, uint32_t b, bool alias) {
+    WRS_CHECK(b < n);
     atomicAdd(hits + (alias ? n + b : b), 1u);
 }
 
@@ -896,6 +905,7 @@ k_two_level_sample(const __grid_constant__ TwoLevelDev tl, DrawGeom g, uint64_t 
         const uint4 tb = ld_bucket(tl.top, mulhi_n32(mix64(c), top_n));
         const double tx = (static_cast<double>(mix64(c + kGolden) >> 11) * 0x1.0p-53) * tl.top_mean;
         const uint32_t grp = pick(tb, tx);
+        WRS_CHECK(grp < tl.groups);
         // the group's own table
         const uint4 lb = ld_bucket(tl.tables[grp],
                                    mulhi_n32(mix64(c + 2 * kGolden), static_cast<uint32_t>(tl.sizes[grp])));
@@ -1098,6 +1108,8 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
     const int sm_unperm = static_cast<int>(plan.tile * sizeof(uint32_t));
     const bool w1 = g.W == 1;
     cudaStream_t ss = on_side ? side : st;
+    poison(B.rec, plan.rec_slots * sizeof(uint2), ss);  // checked builds only
+    poison(B.res, plan.rec_slots * sizeof(uint32_t), ss);
     cudaError_t e = reset_cursors(rg, B, ss);
     if (e != cudaSuccess) return e;
     const unsigned tiles = static_cast<unsigned>(rg.ntiles);
@@ -1338,5 +1350,7 @@ cudaError_t launch_generate_lognormal(double* d_w, uint64_t n, uint64_t offset, 
         d_w, n, offset, rng_key(seed, kLognStream), sigma);
     return cudaGetLastError();
 }
+
+unsigned long long check_failures_sample(unsigned* line) { return tu_check_failures(line); }
 
 }  // namespace wrsb

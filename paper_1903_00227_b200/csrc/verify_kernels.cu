@@ -132,4 +132,6 @@ cudaError_t implied_masses_device(const Bucket* d_b, uint64_t n, double wn, cons
     return e;
 }
 
+unsigned long long check_failures_verify(unsigned* line) { return tu_check_failures(line); }
+
 }  // namespace wrsb

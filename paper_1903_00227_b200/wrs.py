@@ -52,6 +52,7 @@ SIGNATURES = {
     "wrs_verify": (C.c_int, [C.c_char_p, u64, C.c_int]),
     "wrs_b200_default_jobs": (u64, [u64]),
     "wrs_b200_release_cache": (u64, []),
+    "wrs_b200_check_failures": (C.c_int64, [C.POINTER(C.c_uint)]),
     "wrs_b200_weights_from_device": (C.c_int, [vp, u64, C.c_int, C.POINTER(vp)]),
     "wrs_b200_weights_generate_range": (C.c_int, [C.c_char_p, f64, u64, u64, u64, u64,
                                                   C.POINTER(vp)]),
@@ -477,6 +478,13 @@ class MultiSampler:
             self.free()
         except Exception:
             pass
+
+
+def check_failures() -> tuple[int, int]:
+    """(device index-check violations so far, first offending line); (-1, 0)
+    in the normal build (the checks exist only in libwrs_b200_checked.so)."""
+    line = C.c_uint()
+    return int(lib().wrs_b200_check_failures(C.byref(line))), line.value
 
 
 def release_cache() -> int:

@@ -1,4 +1,5 @@
-"""Small-n workload for compute-sanitizer (scripts/gpu_sanitize.sh).
+"""Small-n workload for the checked build (scripts/gpu_checked.sh;
+compute-sanitizer itself is closed on the GPU pool).
 
 Exercises every kernel family of libwrs_b200.so at sizes where the
 sanitizers finish in minutes, and checks each result against the oracle so a
@@ -124,6 +125,9 @@ def main():
     # device power-law deal
     Wp = wrs.Weights.generate("powerlaw", 1.0, 100_003, 8)
     assert np.array_equal(Wp.values(), port.generate_powerlaw(100_003, 1.0, 8))
+    bad, line = wrs.check_failures()
+    print(f"device index-check violations: {bad} (first at line {line})", flush=True)
+    assert bad <= 0, (bad, line)
     print("sanitize cases: all ok", flush=True)
 
 
