@@ -361,7 +361,10 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
 // list positions (a warp row's lights, and its heavies, are consecutive
 // there).  No 40-KB staging buffer and one barrier less per tile; measured at
 // n = 1e8: 0.50 vs 0.53 ms for the staged form.
-__global__ void __launch_bounds__(K1_THREADS, 5)
+#ifndef K1D_MINB
+#define K1D_MINB 5
+#endif
+__global__ void __launch_bounds__(K1_THREADS, K1D_MINB)
 k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
                    unsigned long long* status, double* __restrict__ lw, uint32_t* __restrict__ hidx,
                    double* __restrict__ hw) {
@@ -436,7 +439,10 @@ k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, De
 // K2a / K2c: per-2048-block Neumaier chains, one lane per block
 // ===========================================================================
 constexpr int SCAN_BLOCK = 2048;  // kScanBlock, parallel.hpp:60
-constexpr int K2_WARPS = 2;
+#ifndef K2_WARPS_DEF
+#define K2_WARPS_DEF 2
+#endif
+constexpr int K2_WARPS = K2_WARPS_DEF;
 constexpr int K2_C = 32;          // chunk of each block staged per step
 #ifndef K2_ROW_UNROLL
 #define K2_ROW_UNROLL 4
@@ -1534,7 +1540,10 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* 
 #endif
 constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // 6 CTAs per SM
 constexpr uint32_t K4B_PAD = 64;  // heavy ids staged either side of the tile's own
-__global__ void __launch_bounds__(K1_THREADS)
+#ifndef K4B_MINB
+#define K4B_MINB 1
+#endif
+__global__ void __launch_bounds__(K1_THREADS, K4B_MINB)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
            const unsigned long long* __restrict__ status, const uint32_t* __restrict__ lrank,
            const double* __restrict__ hshare, const uint32_t* __restrict__ hidx,

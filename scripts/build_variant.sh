@@ -1,10 +1,9 @@
-#!/bin/bash
-# A/B builds of libwrs_b200.so with extra nvcc defines, for timing experiments:
-#   bash scripts/build_variant.sh NAME -DFOO=1 ...  -> build_variants/NAME/libwrs_b200.so
-# then WRS_B200_LIB=build_variants/NAME/libwrs_b200.so python bench.py ...
+#!/usr/bin/env bash
+# Build a variant of the library with extra compile flags for A/B timing:
+#   bash scripts/build_variant.sh NAME "-DK4_WARPS_DEF=11 ..."
+# -> build_variants/NAME/libwrs_b200.so (select with WRS_B200_LIB=...)
 set -e
-NAME=$1; shift
-ROOT=$(cd "$(dirname "$0")/.." && pwd)
-D=$ROOT/build_variants/$NAME
-mkdir -p "$D"
-make -s -C "$ROOT/paper_1903_00227_b200/csrc" BUILD="$D/obj" OUT="$D/libwrs_b200.so" NVCC="nvcc $*" -j4
+cd "$(dirname "$0")/.."
+name=$1; shift
+make -s -j8 -C paper_1903_00227_b200/csrc OUT=$PWD/build_variants/$name/libwrs_b200.so \
+    BUILD=$PWD/build_variants/$name/obj EXTRA="$*" all
