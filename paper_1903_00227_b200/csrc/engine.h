@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -34,6 +35,10 @@ size_t release_cache();
 // any GPU and launch shape.
 constexpr uint64_t kJobBucketsMax = 1024, kJobBucketsMin = 32, kJobTarget = 49152;
 inline uint64_t default_job_items(uint64_t n) {
+    if (const char* e = std::getenv("WRS_B200_JOB_ITEMS")) {  // experiments only
+        const uint64_t v = std::strtoull(e, nullptr, 10);
+        if (v >= 1) return v;
+    }
     uint64_t j = kJobBucketsMin;
     while (j < kJobBucketsMax && 2 * j <= n / kJobTarget) j *= 2;
     return j;

@@ -1116,50 +1116,6 @@ k_scan_carry(const DevScalars* sc, const double* __restrict__ totals, double* ca
 // ===========================================================================
 // K3: split points (psa_split, alias.hpp:122-149) -- one thread per split
 // ===========================================================================
-__global__ void __launch_bounds__(256)
-k_split(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__ lpre,
-        const double* __restrict__ hpre, const double* __restrict__ hw, uint32_t* split_l,
-        uint32_t* split_h, double* split_s) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t nl = sc->nl, nh = sc->nh;
-    if (nh == 0) return;  // uniform fill, K4
-    const double wn = sc->wn;
-    if (k == 0) {
-        split_l[0] = 0;
-        split_h[0] = 0;
-        split_s[0] = hw[0];  // carry of job 0 = w(heavy[0]), alias.hpp:219
-        split_l[P] = static_cast<uint32_t>(nl);
-        split_h[P] = static_cast<uint32_t>(nh);
-        split_s[P] = 0.0;
-    }
-    if (k + 1 >= P) return;
-    const uint64_t m = n * (k + 1);
-    const uint64_t np = m / P + (m % P != 0);  // alias.hpp:227
-    const double target = static_cast<double>(np) * wn;
-    uint64_t lo = np > nl ? np - nl : 0;
-    uint64_t hi = np < nh ? np : nh;
-    while (lo < hi) {
-        const uint64_t mid = lo + (hi - lo) / 2;
-        double f;
-        if (mid >= nh)
-            f = CUDART_INF;
-        else
-            f = (__ldg(lpre + (np - mid)) + __ldg(hpre + mid)) + __ldg(hw + mid);
-        if (f > target)
-            hi = mid;
-        else
-            lo = mid + 1;
-    }
-    double spill = 0.0;
-    if (lo < nh) {
-        const double x = (__ldg(hw + lo) + (__ldg(lpre + (np - lo)) + __ldg(hpre + lo))) - target;
-        spill = std_max(0.0, x);
-    }
-    split_l[k + 1] = static_cast<uint32_t>(np - lo);
-    split_h[k + 1] = static_cast<uint32_t>(lo);
-    split_s[k + 1] = spill;
-}
-
 // K3 over checkpointed prefixes (k_scan_blocks_ckpt): the same probe
 // sequence as k_split, each probe decided from a bracket first.  The prefix
 // value at x lies between the values of the checkpoints around it (prefix
@@ -1183,10 +1139,18 @@ __device__ __forceinline__ double ck_value(const CkList& L, uint64_t m) {
 __device__ __forceinline__ double ck_exact(const CkList& L, uint64_t x) {
     if (x == 0) return 0.0;
     const uint64_t e = x - 1;
+    WRS_CHECK(e < L.len);
+    const uint64_t base = e & ~static_cast<uint64_t>(CK_STRIDE - 1);
+    const int cnt = static_cast<int>(e - base) + 1;
+    // all (<= 16) terms in flight at once, then the chain
+    double v[CK_STRIDE];
+#pragma unroll
+    for (int u = 0; u < CK_STRIDE; ++u) v[u] = u < cnt ? __ldg(L.w + base + u) : 0.0;
     const double2 s = __ldg(L.ck + (e / CK_STRIDE));
     CompSumPos cs{s.x, s.y};
-    WRS_CHECK(e < L.len);
-    for (uint64_t p = e & ~static_cast<uint64_t>(CK_STRIDE - 1); p <= e; ++p) cs.add(__ldg(L.w + p));
+#pragma unroll
+    for (int u = 0; u < CK_STRIDE; ++u)
+        if (u < cnt) cs.add(v[u]);
     return cs.value();
 }
 __device__ __forceinline__ void ck_bracket(const CkList& L, uint64_t x, double& lo, double& hi) {
@@ -1199,26 +1163,37 @@ __device__ __forceinline__ void ck_bracket(const CkList& L, uint64_t x, double& 
     hi = (m + 1) * CK_STRIDE < L.len ? ck_value(L, m + 1) * (1.0 + 1e-13) : CUDART_INF;
 }
 
-__global__ void __launch_bounds__(256)
-k_split_ckpt(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restrict__ lw,
-             const double* __restrict__ hw, const double2* __restrict__ lck,
-             const double2* __restrict__ hck, uint32_t* split_l, uint32_t* split_h,
-             double* split_s) {
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t nl = sc->nl, nh = sc->nh;
-    if (nh == 0) return;  // uniform fill, K4
-    const double wn = sc->wn;
-    if (k == 0) {
-        split_l[0] = 0;
-        split_h[0] = 0;
-        split_s[0] = hw[0];  // carry of job 0 = w(heavy[0]), alias.hpp:219
-        split_l[P] = static_cast<uint32_t>(nl);
-        split_h[P] = static_cast<uint32_t>(nh);
-        split_s[P] = 0.0;
-    }
-    if (k + 1 >= P) return;
-    const CkList Lc{lw, lck, nl}, Hc{hw, hck, nh};
-    const uint64_t m = n * (k + 1);
+// Where the prefix values K3 probes come from: the full prefix arrays
+// (k_scan_blocks<true>) or the checkpoints (k_scan_blocks_ckpt).
+struct SplitSrc {
+    const double* lpre;
+    const double* hpre;
+    CkList L, H;
+    const double* hw;
+    bool ckpt;
+};
+
+struct Boundary {
+    uint32_t i, j;
+    double spill;
+};
+
+// Boundary b of psa_plan (alias.hpp:214-238): b = 0 -> (0, 0, w(heavy[0]));
+// b = P -> (nl, nh, 0); else psa_split (alias.hpp:122-149) after the first
+// n' = ceil(n b / P) buckets, with the reference's probe sequence.  With
+// checkpoints every probe is decided from a bracket first: the prefix value
+// at x lies between the values of the checkpoints around it (prefix values of
+// non-negative terms only grow, up to rounding: each is within a few ulps of
+// the exact prefix sum), widened by 1e-13 relative; rounding is monotone, so
+// f(mid) = (L + H) + w lies between the same expressions of the bracket ends.
+// Only when the target falls inside does the probe recompute the exact L
+// and H (the checkpoint state plus <= 16 compensated adds, the additions
+// k_scan_blocks<true> makes).  Results are identical either way.
+__device__ __forceinline__ Boundary psa_boundary(uint64_t b, uint64_t n, uint64_t P, uint64_t nl,
+                                                 uint64_t nh, double wn, const SplitSrc& S) {
+    if (b == 0) return Boundary{0u, 0u, __ldg(S.hw)};  // carry of job 0 = w(heavy[0]), alias.hpp:219
+    if (b >= P) return Boundary{static_cast<uint32_t>(nl), static_cast<uint32_t>(nh), 0.0};
+    const uint64_t m = n * b;
     const uint64_t np = m / P + (m % P != 0);  // alias.hpp:227
     const double target = static_cast<double>(np) * wn;
     uint64_t lo = np > nl ? np - nl : 0;
@@ -1229,16 +1204,19 @@ k_split_ckpt(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restr
         if (mid >= nh) {
             above = true;  // f = inf
         } else {
-            const double w = __ldg(hw + mid);
-            double l0, l1, h0, h1;
-            ck_bracket(Lc, np - mid, l0, l1);
-            ck_bracket(Hc, mid, h0, h1);
-            if ((l0 + h0) + w > target) {
-                above = true;
-            } else if ((l1 + h1) + w <= target) {
-                above = false;
+            const double w = __ldg(S.hw + mid);
+            if (!S.ckpt) {
+                above = (__ldg(S.lpre + (np - mid)) + __ldg(S.hpre + mid)) + w > target;
             } else {
-                above = (ck_exact(Lc, np - mid) + ck_exact(Hc, mid)) + w > target;
+                double l0, l1, h0, h1;
+                ck_bracket(S.L, np - mid, l0, l1);
+                ck_bracket(S.H, mid, h0, h1);
+                if ((l0 + h0) + w > target)
+                    above = true;
+                else if ((l1 + h1) + w <= target)
+                    above = false;
+                else
+                    above = (ck_exact(S.L, np - mid) + ck_exact(S.H, mid)) + w > target;
             }
         }
         if (above)
@@ -1248,12 +1226,27 @@ k_split_ckpt(uint64_t n, uint64_t P, const DevScalars* sc, const double* __restr
     }
     double spill = 0.0;
     if (lo < nh) {
-        const double x = (__ldg(hw + lo) + (ck_exact(Lc, np - lo) + ck_exact(Hc, lo))) - target;
-        spill = std_max(0.0, x);
+        const double sig = S.ckpt ? ck_exact(S.L, np - lo) + ck_exact(S.H, lo)
+                                  : __ldg(S.lpre + (np - lo)) + __ldg(S.hpre + lo);
+        spill = std_max(0.0, (__ldg(S.hw + lo) + sig) - target);
     }
-    split_l[k + 1] = static_cast<uint32_t>(np - lo);
-    split_h[k + 1] = static_cast<uint32_t>(lo);
-    split_s[k + 1] = spill;
+    return Boundary{static_cast<uint32_t>(np - lo), static_cast<uint32_t>(lo), spill};
+}
+
+// K3 as its own kernel (the pack computes the boundaries itself by default;
+// WRS_B200_K3=separate): one thread per boundary.
+__global__ void __launch_bounds__(256)
+k_split(uint64_t n, uint64_t P, const DevScalars* sc, SplitSrc S, uint32_t* split_l,
+        uint32_t* split_h, double* split_s) {
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    if (nh == 0 || b > P) return;  // uniform fill, K4
+    S.L.len = nl;
+    S.H.len = nh;
+    const Boundary r = psa_boundary(b, n, P, nl, nh, sc->wn, S);
+    split_l[b] = r.i;
+    split_h[b] = r.j;
+    split_s[b] = r.spill;
 }
 
 // ===========================================================================
@@ -1277,7 +1270,7 @@ constexpr int K4_S = 14;          // steps per phase (items consumed per list <=
 constexpr int K4_R = 32;          // ring slots per list (power of two, >= 2S + 4)
 constexpr int K4_RS = K4_R + 2;   // row stride in doubles (16-B aligned rows for the pair copies)
 #ifndef K4_WARPS_DEF
-#define K4_WARPS_DEF 12           // 17.6 KB of rings per warp: 12 warps fill 211 KB
+#define K4_WARPS_DEF 11           // 17.6 KB of rings per warp (11: 0.66 vs 0.67 ms for 12)
 #endif
 constexpr int K4_WARPS = K4_WARPS_DEF;
 static_assert(2 * K4_S + 4 <= K4_R, "a refill must not reach the slots of unflushed outputs");
@@ -1541,7 +1534,7 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* 
 constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // 6 CTAs per SM
 constexpr uint32_t K4B_PAD = 64;  // heavy ids staged either side of the tile's own
 #ifndef K4B_MINB
-#define K4B_MINB 1
+#define K4B_MINB 6
 #endif
 __global__ void __launch_bounds__(K1_THREADS, K4B_MINB)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
@@ -1799,7 +1792,6 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
     const unsigned k2_grid = static_cast<unsigned>((nblocks + K2_WARPS * 32 - 1) / (K2_WARPS * 32));
-    const unsigned k3_grid = static_cast<unsigned>((P + 255) / 256);
     const unsigned k4_grid = static_cast<unsigned>((P + k4_warps * 32 - 1) / (k4_warps * 32));
     cudaError_t e;
 #define REC(i)                                          \
@@ -1876,12 +1868,12 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
         K2_LAUNCH(true);
 #undef K2_LAUNCH
     REC(4);
-    if (ws.ckpt)
-        k_split_ckpt<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lw, ws.hw, ws.lck, ws.hck, ws.split_l,
-                                              ws.split_h, ws.split_s);
-    else
-        k_split<<<k3_grid, 256, 0, st>>>(n, P, ws.sc, ws.lpre, ws.hpre, ws.hw, ws.split_l,
-                                         ws.split_h, ws.split_s);
+    {
+        SplitSrc src{ws.lpre, ws.hpre, CkList{ws.lw, ws.lck, 0}, CkList{ws.hw, ws.hck, 0}, ws.hw,
+                     ws.ckpt};
+        const unsigned grid = static_cast<unsigned>((P + 1 + 255) / 256);
+        k_split<<<grid, 256, 0, st>>>(n, P, ws.sc, src, ws.split_l, ws.split_h, ws.split_s);
+    }
     REC(5);
     if (pos)  // W < 1e300: the remainder stays finite
         k_pack<true><<<k4_grid, k4_warps * 32, k4_smem, st>>>(
