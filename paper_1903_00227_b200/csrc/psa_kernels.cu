@@ -364,6 +364,9 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
 #ifndef K1D_MINB
 #define K1D_MINB 5
 #endif
+#ifndef K1_LOOKBACK_WIN
+#define K1_LOOKBACK_WIN 1  // look-back windows of 32 tiles per round (measured: 2, 4, 8 are slower)
+#endif
 __global__ void __launch_bounds__(K1_THREADS, K1D_MINB)
 k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
                    unsigned long long* status, double* __restrict__ lw, uint32_t* __restrict__ hidx,
@@ -386,26 +389,42 @@ k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, De
             if (lane == 0) st_volatile(&status[0], FLAG_P | totL);
         } else {
             if (lane == 0) st_volatile(&status[tile], FLAG_A | totL);
+            // 128 predecessors per round (4 per lane): with hundreds of tiles
+            // in flight the inclusive prefixes lag far behind, and a round is
+            // one memory latency
+            constexpr int LB = K1_LOOKBACK_WIN;
             long long p = static_cast<long long>(tile) - 1;
             while (true) {
-                const long long idx = p - lane;
-                unsigned long long v = FLAG_P;
-                if (idx >= 0) {
-                    do {
-                        v = ld_volatile(&status[idx]);
-                    } while ((v >> 62) == 0);
-                }
-                const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-                unsigned long long c = v & VAL_MASK;
-                if (pm) {
-                    const int first = __ffs(pm) - 1;
-                    if (lane > first) c = 0;
+                unsigned long long v[LB];
+#pragma unroll
+                for (int u = 0; u < LB; ++u) {
+                    const long long idx = p - (u * 32 + lane);
+                    v[u] = FLAG_P;
+                    if (idx >= 0) v[u] = ld_volatile(&status[idx]);
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-                excl += c;
-                if (pm) break;
-                p -= 32;
+                for (int u = 0; u < LB; ++u) {
+                    const long long idx = p - (u * 32 + lane);
+                    while ((v[u] >> 62) == 0) v[u] = ld_volatile(&status[idx]);
+                }
+                bool done = false;
+#pragma unroll
+                for (int u = 0; u < LB; ++u) {
+                    if (!done) {
+                        const unsigned pm = __ballot_sync(0xffffffffu, (v[u] >> 62) == 2);
+                        unsigned long long c = v[u] & VAL_MASK;
+                        if (pm) {
+                            const int first = __ffs(pm) - 1;
+                            if (lane > first) c = 0;
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                        excl += c;
+                        done = pm != 0;
+                    }
+                }
+                if (done) break;
+                p -= 32 * LB;
             }
             if (lane == 0) st_volatile(&status[tile], FLAG_P | (excl + totL));
         }

@@ -562,3 +562,14 @@ def test_masses_agree_with_reference_vose_and_sweep(P):
             rm = R.implied_masses(b, wn)
             assert np.max(np.abs(rm - w) / w) < 1e-9, method
             assert np.max(np.abs(rm - gm) / w) < 2e-9, method
+
+
+def test_psa_exact_env_gives_the_reference_table(P, monkeypatch):
+    """WRS_B200_PSA_EXACT=1: an unmodified client's wrs_sampler_build(w, "psa",
+    workers) gets the reference's AliasTable(wt, psa, workers) and stream."""
+    monkeypatch.setenv("WRS_B200_PSA_EXACT", "1")
+    w = P.generate_powerlaw(50_000, 1.0, 3)
+    W = wrs.Weights.from_array(w)
+    S = wrs.Sampler.build(W, "psa", 8)
+    assert S.jobs == 8
+    assert_same_table(S, w, 8, P)
