@@ -1149,6 +1149,26 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
     return cudaGetLastError();
 }
 
+// Draws per region pass for a plain draw of cnt draws: every pass sweeps the
+// whole table once more (16 GB at n = 1e9), so big draws take passes of up to
+// 2^31 draws when the scratch (12 B per draw) fits comfortably in free device
+// memory, else 2^30 (or what WRS_B200_DRAW_CHUNK says).
+static uint64_t draw_chunk_for(const DrawGeom& g, uint64_t cnt, const SampleWorkspace* ws) {
+    if (getenv("WRS_B200_DRAW_CHUNK")) return region_chunk_max();
+    uint64_t chunk = 1ull << 30;
+    if (cnt > chunk) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const uint64_t big = cnt < (1ull << 31) ? cnt : (1ull << 31);
+            const RegionPlan p = plan_regions(g, big);
+            if (region_bytes(p, big, nullptr, nullptr) < 0.6 * (free_b + ws->bytes)) chunk = big;
+        } else {
+            cudaGetLastError();
+        }
+    }
+    return chunk;
+}
+
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
                           uint64_t stream_id, uint64_t q_begin, uint64_t q_end, uint64_t k,
                           uint32_t workers, uint32_t base, uint32_t* d_out, cudaStream_t st,
@@ -1172,7 +1192,7 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
                                                                                q_end, base, d_out);
         return cudaGetLastError();
     }
-    const uint64_t chunk_max = region_chunk_max();
+    const uint64_t chunk_max = draw_chunk_for(g, cnt, ws);
     const uint64_t chunk = cnt < chunk_max ? cnt : chunk_max;
     RegionPlan plan = plan_regions(g, chunk);
     cudaError_t e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr));

@@ -131,3 +131,23 @@ def test_size_sweep_top_tables(Z, tag, dist, param):
     S = wrs.Sampler.build_psa(W, P)
     assert S.bucket_mean == float(Z[f"{tag}/P{P}/bucket_mean"])
     assert sha(S.buckets()) == str(Z[f"{tag}/P{P}/buckets_sha"])
+
+
+def test_draws_beyond_one_pass_bit_exact():
+    """A draw of more than 2^30 samples takes region passes of up to 2^31
+    draws when memory allows (fewer sweeps of the table): windows across the
+    pass boundaries are bit-exact against the oracle, for W = 1 and W = 7."""
+    import torch
+    import oracle
+    P = oracle.port()
+    n, k = 20_000_003, (1 << 30) + 123_456_789
+    W = wrs.Weights.generate("uniform", 0.0, n, 5)
+    S = wrs.Sampler.build(W, "psa", 1)
+    b = S.buckets()
+    out = torch.empty(k, dtype=torch.int32, device="cuda")
+    for Wk in (1, 7):
+        S.draw_device(31, k, Wk, out)
+        torch.cuda.synchronize()
+        for lo in (0, (1 << 30) - 50_000, k - 100_000):
+            ref = P.sample_range(b, S.bucket_mean, 31, k, Wk, lo, lo + 100_000)
+            assert np.array_equal(out[lo:lo + 100_000].cpu().numpy().view(np.uint32), ref), (Wk, lo)
