@@ -1349,34 +1349,25 @@ __device__ __forceinline__ void k4_rows(K4Rings& R, const double* __restrict__ l
 #pragma unroll
         for (int ps = 0; ps < PASSES; ++ps) {
             const uint32_t off = q2 + 16u * ps;
-            // flush
+            // flush, branch-free: the pair is read whole (one 16-B load), then
+            // one of three predicated stores (both elements / first / second)
             {
                 const uint32_t b = (d.x & ~1u) + off;
                 const bool v0 = b >= d.x && b < fle, v1 = b + 1 < fle;
-                if (v0 || v1) {
-                    const uint32_t s = b & (K4_R - 1);
-                    const uint32_t r0 = low_word(Lr[s]), r1 = low_word(Lr[s + 1]);
-                    if (v0 && v1)
-                        *reinterpret_cast<uint2*>(lrank + b) = make_uint2(r0, r1);
-                    else if (v0)
-                        lrank[b] = r0;
-                    else
-                        lrank[b + 1] = r1;
-                }
+                const double2 pr = *reinterpret_cast<const double2*>(&Lr[b & (K4_R - 1)]);
+                const uint32_t r0 = static_cast<uint32_t>(__double_as_longlong(pr.x));
+                const uint32_t r1 = static_cast<uint32_t>(__double_as_longlong(pr.y));
+                if (v0 && v1) *reinterpret_cast<uint2*>(lrank + b) = make_uint2(r0, r1);
+                if (v0 && !v1) lrank[b] = r0;
+                if (!v0 && v1) lrank[b + 1] = r1;
             }
             {
                 const uint32_t b = (d.y & ~1u) + off;
                 const bool v0 = b >= d.y && b < fhe, v1 = b + 1 < fhe;
-                if (v0 || v1) {
-                    const uint32_t s = b & (K4_R - 1);
-                    const double s0 = Hr[s], s1 = Hr[s + 1];
-                    if (v0 && v1)
-                        *reinterpret_cast<double2*>(hshare + b) = make_double2(s0, s1);
-                    else if (v0)
-                        hshare[b] = s0;
-                    else
-                        hshare[b + 1] = s1;
-                }
+                const double2 pr = *reinterpret_cast<const double2*>(&Hr[b & (K4_R - 1)]);
+                if (v0 && v1) *reinterpret_cast<double2*>(hshare + b) = pr;
+                if (v0 && !v1) hshare[b] = pr.x;
+                if (!v0 && v1) hshare[b + 1] = pr.y;
             }
             // refill (pairs; the inputs have >= 64 B of slack past their ends)
             {
