@@ -1289,7 +1289,7 @@ constexpr int K4_S = 14;          // steps per phase (items consumed per list <=
 constexpr int K4_R = 32;          // ring slots per list (power of two, >= 2S + 4)
 constexpr int K4_RS = K4_R + 2;   // row stride in doubles (16-B aligned rows for the pair copies)
 #ifndef K4_WARPS_DEF
-#define K4_WARPS_DEF 11           // 17.6 KB of rings per warp (11: 0.66 vs 0.67 ms for 12)
+#define K4_WARPS_DEF 12           // 17.6 KB of rings per warp: 12 warps fill 211 KB
 #endif
 constexpr int K4_WARPS = K4_WARPS_DEF;
 static_assert(2 * K4_S + 4 <= K4_R, "a refill must not reach the slots of unflushed outputs");
@@ -1326,6 +1326,10 @@ __device__ __forceinline__ void cp_async16_ordered(void* smem, const void* gmem)
 //           32 back, whose output this same pass has already read).
 // A refill may target a slot a flush of the same row reads in the same
 // iteration: the flush's loads feed its stores, which issue before the copy.
+#ifndef K4R_UNROLL
+#define K4R_UNROLL 4
+#endif
+constexpr int K4R_U = K4R_UNROLL;  // row iterations unrolled
 template <int PASSES>
 __device__ __forceinline__ void k4_rows(K4Rings& R, const double* __restrict__ lw,
                                         const double* __restrict__ hw, uint32_t* __restrict__ lrank,
@@ -1333,7 +1337,7 @@ __device__ __forceinline__ void k4_rows(K4Rings& R, const double* __restrict__ l
     const int lane = threadIdx.x & 31;
     const uint32_t q2 = 2u * (lane & 7);
     const int quarter = lane >> 3;
-#pragma unroll 2
+#pragma unroll K4R_U
     for (int t = 0; t < 8; ++t) {
         const int r = 4 * t + quarter;
         const uint4 d = R.pos[r];
