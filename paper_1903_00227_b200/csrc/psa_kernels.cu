@@ -622,9 +622,9 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
         cp_async_commit();
     };
 
+    load_chunk(0, 0);  // first chunk in flight while the carry arrives
     CompSumPos cs{0.0, 0.0};
-    if (me.len > 0) cs.add(carries[b]);  // run.add(carry[b]) = (carry, 0), parallel.hpp:124
-    load_chunk(0, 0);
+    if (me.len > 0) cs.add(__ldg(carries + b));  // run.add(carry[b]) = (carry, 0), parallel.hpp:124
     for (int c = 0; c < nchunks; ++c) {
         const int buf = c & 1;
         if (c + 1 < nchunks) {
