@@ -1,7 +1,10 @@
 """One build + one device draw of k samples at table size n, for launch-list
 profiling of the draw kernels at sizes other than the bench's:
     ncu --metrics gpu__time_duration.sum python scripts/draw_probe.py n k"""
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 
