@@ -662,6 +662,105 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
     }
 }
 
+// K2a with TMA bulk copies (experiment, WRS_B200_K2_BULK=1): each warp's
+// lane 0 moves the warp's 32 block-chunk rows (256 B each, contiguous in
+// global memory) with cp.async.bulk into 16-B-aligned shared rows, completion
+// counted on a per-warp, per-buffer mbarrier; the lanes then read their rows
+// as 16-B pairs (conflict-free at a 34-double row stride).
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n"
+        ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                   "r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+
+template <class CS>
+__global__ void __launch_bounds__(K2_WARPS * 32)
+k_scan_totals_bulk(const double* __restrict__ lw, const double* __restrict__ hw, const DevScalars* sc,
+                   double* __restrict__ totals) {
+    __shared__ __align__(16) double tile[K2_WARPS][2][32][K2_C + 2];
+    __shared__ K2Lane lanes[K2_WARPS][32];
+    __shared__ __align__(8) uint64_t mbar[K2_WARPS][2];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t b = (static_cast<uint64_t>(blockIdx.x) * K2_WARPS + wq) * 32 + lane;
+    K2Lane me{nullptr, nullptr, 0};
+    if (b < nbl) {
+        me.src = lw + b * SCAN_BLOCK;
+        me.len = static_cast<int>(umin64(SCAN_BLOCK, nl - b * SCAN_BLOCK));
+    } else if (b - nbl < nbh) {
+        const uint64_t hb = b - nbl;
+        me.src = hw + hb * SCAN_BLOCK;
+        me.len = static_cast<int>(umin64(SCAN_BLOCK, nh - hb * SCAN_BLOCK));
+    }
+    lanes[wq][lane] = me;
+    int maxlen = me.len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    if (maxlen == 0) return;
+    if (lane == 0) {
+        mbar_init(&mbar[wq][0], 1);
+        mbar_init(&mbar[wq][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int nchunks = (maxlen + K2_C - 1) / K2_C;
+    auto load_chunk = [&](int c, int buf) {
+        if (lane == 0) {
+            unsigned total = 0;
+            for (int r = 0; r < 32; ++r) {
+                const int len = lanes[wq][r].len - c * K2_C;
+                if (len > 0) total += ((min(len, K2_C) * 8 + 15) & ~15);
+            }
+            mbar_expect(&mbar[wq][buf], total);
+            for (int r = 0; r < 32; ++r) {
+                const K2Lane L = lanes[wq][r];
+                const int len = L.len - c * K2_C;
+                if (len > 0)
+                    bulk_g2s(&tile[wq][buf][r][0], L.src + c * K2_C,
+                             (min(len, K2_C) * 8 + 15) & ~15, &mbar[wq][buf]);
+            }
+        }
+    };
+    CS cs{0.0, 0.0};
+    unsigned phase[2] = {0, 0};
+    load_chunk(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) load_chunk(c + 1, buf ^ 1);
+        mbar_wait(&mbar[wq][buf], phase[buf]);
+        phase[buf] ^= 1;
+        const int cnt = min(K2_C, me.len - c * K2_C);
+        const double2* row = reinterpret_cast<const double2*>(tile[wq][buf][lane]);
+        if (cnt == K2_C) {
+#pragma unroll
+            for (int e = 0; e < K2_C / 2; ++e) {
+                const double2 v = row[e];
+                cs.add(v.x);
+                cs.add(v.y);
+            }
+        } else {
+            const double* r1 = tile[wq][buf][lane];
+            for (int e = 0; e < cnt; ++e) cs.add(r1[e]);
+        }
+        __syncwarp();
+    }
+    if (me.len > 0) totals[b] = cs.value();  // carry[b] = local.value(), parallel.hpp:114
+}
+
 // Small tables (a few block chains per SM, so the chains' latency is the
 // kernel's time): one lane per block as above, but the block is read straight
 // into registers with 16-B loads, the next 32 elements in flight while the
@@ -1865,7 +1964,11 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
             k_scan_blocks<PASS3, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(                     \
                 ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
     } while (0)
-    K2_LAUNCH(false);
+    if (pos && !split && !direct && std::getenv("WRS_B200_K2_BULK"))
+        k_scan_totals_bulk<CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.sc,
+                                                                          ws.totals);
+    else
+        K2_LAUNCH(false);
     REC(2);
     if (pos)
         k_scan_carry_split<<<2, 160, K2W_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
