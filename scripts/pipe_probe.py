@@ -1,7 +1,10 @@
 """Draw-stage chunk pipeline sweep: 1e9 draws from an n-item table with
 WRS_B200_DRAW_PIPE set to each configuration on the command line, timed with
 CUDA events (median of 5) and checked byte-equal to the unpipelined draw.
-    python scripts/pipe_probe.py 1e8 1e9 1 2,2,3,2 4,2,3,2 ..."""
+    python scripts/pipe_probe.py 1e8 1e9 1 2,2,3,2 4,2,3,2 ...
+The pipeline was measured slower and reverted (profiles/r02_draw_pipeline_
+experiment.md); the library now ignores WRS_B200_DRAW_PIPE, so this times the
+shipped serial plan unless run against that experiment's build."""
 import hashlib
 import os
 import statistics
