@@ -31,6 +31,8 @@ struct DevScalars {
     unsigned long long nl, nh;     // light / heavy counts (alias.hpp:41-46)
     unsigned int tile_counter;     // K1 dynamic tile ids
     unsigned int plan_error;       // psa_plan's logic_error (alias.hpp:230-231)
+    unsigned int k2_ticket;        // fused K2b+K2c: CTA roles in start order
+    unsigned int k2_work;          // fused K2b+K2c: next checkpoint warp unit
 };
 
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;  // rng.hpp:23

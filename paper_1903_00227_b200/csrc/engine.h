@@ -57,6 +57,7 @@ struct Workspace {
     double* node_val = nullptr;      // K0 pairwise tree nodes above the CTA cut
     unsigned* node_cnt = nullptr;    // K0 arrival counters
     unsigned long long* tile_status = nullptr;  // K1 decoupled look-back
+    unsigned* k2_flags = nullptr;  // fused K2b+K2c: per list, one 128-B line per published chunk
     uint32_t* hidx = nullptr;        // heavy item ids, ascending (light ids stay implicit)
     double* lw = nullptr;            // gathered light weights
     double* hw = nullptr;            // gathered heavy weights

@@ -580,17 +580,42 @@ k_scan_blocks(const double* __restrict__ lw, const double* __restrict__ hw,
 // (blocks are multiples of 16); the state at a block start is run.add(carry)
 // = (carry, 0) exactly (parallel.hpp:124).
 constexpr int CK_STRIDE = 16;
-__global__ void __launch_bounds__(K2_WARPS * 32)
-k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
-                   double2* __restrict__ lck, double2* __restrict__ hck, const DevScalars* sc,
-                   const double* __restrict__ carries) {
-    __shared__ double tile[K2_WARPS][2][32][K2_C + 1];
-    __shared__ K2Lane lanes[K2_WARPS][32];
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+typedef double K2Tile[2][32][K2_C + 1];  // one warp's double-buffered block chunks
+
+// acquire load of a progress counter published by another CTA
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Fused K2b+K2c publication flags: per list, one word per chunk of K2F_S
+// carries, each on its own 128-B line so the waiting warps poll many lines
+// rather than one.  nb_flags = chunk slots per list.
+constexpr int K2F_S = 256;  // totals per chain chunk (publication granularity)
+__host__ __device__ inline uint64_t k2_flag_slots(uint64_t n) {
+    return ((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 2 + K2F_S - 1) / K2F_S + 1;
+}
+__host__ __device__ inline uint64_t k2_flag_words(uint64_t n) { return 2 * 32 * k2_flag_slots(n); }
+__device__ __forceinline__ const unsigned* k2_flag(const unsigned* f, bool heavy, uint64_t slots,
+                                                   uint64_t chunk) {
+    return f + 32 * ((heavy ? slots : 0) + chunk);
+}
+
+// One warp's 32 block chains of K2c (warp unit `wu` of the launch).  done
+// (fused K2b+K2c only): per list, how many carries the chain has published;
+// the lane waits for its block's before reading it (the chunk loads are
+// already in flight).
+__device__ __forceinline__ void ckpt_warp(uint64_t wu, K2Tile& tile, K2Lane* lanes,
+                                          const double* __restrict__ lw, const double* __restrict__ hw,
+                                          double2* __restrict__ lck, double2* __restrict__ hck,
+                                          const DevScalars* sc, const double* carries,
+                                          const unsigned* done, uint64_t nb_flags) {
+    const int lane = threadIdx.x & 31;
     const uint64_t nl = sc->nl, nh = sc->nh;
     const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
     const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
-    const uint64_t b = (static_cast<uint64_t>(blockIdx.x) * K2_WARPS + wq) * 32 + lane;
+    const uint64_t b = wu * 32 + lane;
 
     K2Lane me{nullptr, nullptr, 0};
     double2* ck = nullptr;
@@ -604,7 +629,7 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
         ck = hck + hb * (SCAN_BLOCK / CK_STRIDE);
         me.len = static_cast<int>(umin64(SCAN_BLOCK, nh - hb * SCAN_BLOCK));
     }
-    lanes[wq][lane] = me;
+    lanes[lane] = me;
     int maxlen = me.len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
@@ -615,16 +640,30 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
     auto load_chunk = [&](int c, int buf) {
 #pragma unroll K2_ROW_U
         for (int r = 0; r < 32; ++r) {
-            const K2Lane L = lanes[wq][r];
+            const K2Lane L = lanes[r];
             const int e = c * K2_C + lane;
-            if (e < L.len) cp_async8(&tile[wq][buf][r][lane], L.src + e);
+            if (e < L.len) cp_async8(&tile[buf][r][lane], L.src + e);
         }
         cp_async_commit();
     };
 
     load_chunk(0, 0);  // first chunk in flight while the carry arrives
     CompSumPos cs{0.0, 0.0};
-    if (me.len > 0) cs.add(__ldg(carries + b));  // run.add(carry[b]) = (carry, 0), parallel.hpp:124
+    if (me.len > 0) {
+        double carry;
+        if (done) {  // published by the chain CTA of this launch: acquire, then an L2 load
+            const bool heavy = b >= nbl;
+            const unsigned* f = k2_flag(done, heavy, nb_flags, (heavy ? b - nbl : b) / K2F_S);
+            // relaxed polls (an acquire per poll invalidates the SM's L1 each
+            // time), one acquire fence once the flag is seen
+            while (*reinterpret_cast<const volatile unsigned*>(f) == 0) __nanosleep(128);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            carry = __ldcg(carries + b);
+        } else {
+            carry = __ldg(carries + b);
+        }
+        cs.add(carry);  // run.add(carry[b]) = (carry, 0), parallel.hpp:124
+    }
     for (int c = 0; c < nchunks; ++c) {
         const int buf = c & 1;
         if (c + 1 < nchunks) {
@@ -635,7 +674,7 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
         }
         __syncwarp();
         const int cnt = min(K2_C, me.len - c * K2_C);
-        const double* row = tile[wq][buf][lane];
+        const double* row = tile[buf][lane];
         if (cnt > 0) {
             // the two checkpoints of this 32-element chunk: one full 32-B sector
             double2 k0, k1;
@@ -660,6 +699,17 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
         }
         __syncwarp();
     }
+}
+
+__global__ void __launch_bounds__(K2_WARPS * 32)
+k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
+                   double2* __restrict__ lck, double2* __restrict__ hck, const DevScalars* sc,
+                   const double* __restrict__ carries) {
+    __shared__ K2Tile tile[K2_WARPS];
+    __shared__ K2Lane lanes[K2_WARPS][32];
+    const int wq = threadIdx.x >> 5;
+    ckpt_warp(static_cast<uint64_t>(blockIdx.x) * K2_WARPS + wq, tile[wq], lanes[wq], lw, hw, lck,
+              hck, sc, carries, nullptr, 0);
 }
 
 // K2a with TMA bulk copies (experiment, WRS_B200_K2_BULK=1): each warp's
@@ -1040,13 +1090,22 @@ k_scan_blocks_split(const double* __restrict__ lw, const double* __restrict__ hw
 // issued by one warp (chain_bench: 8.3 vs 22 cycles).  The same additions as
 // CompSumPos::add, in the same order: carries are bit-identical.
 constexpr int K2W_S = 1024;               // totals per chunk
-constexpr int K2W_SMEM = 11 * K2W_S * 8 + 4 * 8;  // x ring 3, T ring 4, e ring 2, L ring 2, hin ring 4
-__global__ void __launch_bounds__(160)
-k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, double* carries,
-                   double* lpre, double* hpre) {
-    extern __shared__ __align__(16) double k2w[];
-    double* X = k2w;             // [3][S] totals
-    double* T = X + 3 * K2W_S;   // [4][S] hi after each add
+// x ring RX, T ring 4, e ring 2, L ring 2, hin ring 4
+__host__ __device__ constexpr int k2w_smem(int S, int RX) { return (RX + 8) * S * 8 + 4 * 8; }
+constexpr int K2W_SMEM = k2w_smem(K2W_S, 3);
+// The chain of one list (heavy: the heavy list) over chunks of S totals, the
+// totals prefetched D chunks ahead into a ring of RX >= D + 2 buffers (chunk c
+// is read in steps c and c + 1).  done (fused K2b+K2c only): the flag line
+// of chunk c is released one step after its carries were stored, so the
+// fence finds the stores complete instead of stalling the chain.
+template <int K2W_S, int D = 1, int RX = 3>
+__device__ __forceinline__ void carry_chain(bool heavy, double* k2w, const DevScalars* sc,
+                                            const double* __restrict__ totals, double* carries,
+                                            double* lpre, double* hpre, unsigned* done,
+                                            uint64_t nb_flags) {
+    static_assert(RX >= D + 2, "x ring too short for the prefetch depth");
+    double* X = k2w;             // [RX][S] totals
+    double* T = X + RX * K2W_S;  // [4][S] hi after each add
     double* E = T + 4 * K2W_S;   // [2][S] error terms
     double* L = E + 2 * K2W_S;   // [2][S] lo before each add
     double* hin = L + 2 * K2W_S;  // [4] hi entering each chunk
@@ -1054,7 +1113,6 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
     const uint64_t nl = sc->nl, nh = sc->nh;
     const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
     const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
-    const bool heavy = blockIdx.x == 1;
     const uint64_t nb = heavy ? nbh : nbl;
     const uint64_t off = heavy ? nbl : 0;
     if (threadIdx.x == 0) (heavy ? hpre : lpre)[0] = 0.0;  // prefix[0] = 0, alias.hpp:89
@@ -1068,7 +1126,7 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
     auto load = [&](int c) {
         if (c < nch) {
             const int cnt = cnt_of(c);
-            double* xb = X + (c % 3) * K2W_S;
+            double* xb = X + (c % RX) * K2W_S;
             for (int i = lane; i < cnt; i += 32)
                 cp_async8(xb + i, src + static_cast<uint64_t>(c) * K2W_S + i);
         }
@@ -1080,25 +1138,36 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
     };
     double hi = 0.0, lo = 0.0;  // warp 1 / warp 3, lane 0
     if (warp == 0) {
-        load(0);
-        cp_async_wait<0>();
+#pragma unroll
+        for (int d = 0; d < D; ++d) load(d);
+        cp_async_wait<D - 1>();  // chunk 0 landed
     }
     __syncthreads();
-    for (int it = 0; it < nch + 3; ++it) {
+    const int steps = nch + 3 + (done ? 1 : 0);  // + the last chunk's publication
+    for (int it = 0; it < steps; ++it) {
         if (warp == 0) {
-            load(it + 1);  // read by warp 1 next step
+            load(it + D);  // read by warp 1 D steps from now
         } else if (warp == 1) {
             const int c = it;
             if (c < nch && lane == 0) {
                 const int cnt = cnt_of(c);
-                const double* __restrict__ xb = X + (c % 3) * K2W_S;
+                const double* __restrict__ xb = X + (c % RX) * K2W_S;
                 double* __restrict__ tb = T + (c % 4) * K2W_S;
                 hin[c % 4] = hi;
                 int k = 0;
-                for (; k + 16 <= cnt; k += 16) {  // loads first: the rings never alias
-                    double x[16];
+                // 16 at a time, the next 16 loaded while these add (the rings
+                // never alias): the chain runs at the DADD latency
+                double x[16];
+                if (cnt >= 16) {
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) x[u] = xb[k + u];
+                    for (int u = 0; u < 16; ++u) x[u] = xb[u];
+                }
+                for (; k + 16 <= cnt; k += 16) {
+                    // (past the chunk's end these read the next ring buffer or
+                    // T, inside the allocation; the values go unused)
+                    double y[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) y[u] = xb[k + 16 + u];
 #pragma unroll
                     for (int u = 0; u < 16; ++u) {
                         hi = hi + x[u];
@@ -1106,6 +1175,8 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
                     }
 #pragma unroll
                     for (int u = 0; u < 16; ++u) tb[k + u] = x[u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) x[u] = y[u];
                 }
                 for (; k < cnt; ++k) {
                     hi = hi + xb[k];
@@ -1116,7 +1187,7 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
             const int c = it - 1;
             if (c >= 0 && c < nch) {
                 const int cnt = cnt_of(c);
-                const double* xb = X + (c % 3) * K2W_S;
+                const double* xb = X + (c % RX) * K2W_S;
                 const double* tb = T + (c % 4) * K2W_S;
                 double* eb = E + (c % 2) * K2W_S;
                 for (int k = lane; k < cnt; k += 32) {
@@ -1133,10 +1204,15 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
                 const double* __restrict__ eb = E + (c % 2) * K2W_S;
                 double* __restrict__ lb = L + (c % 2) * K2W_S;
                 int k = 0;
-                for (; k + 16 <= cnt; k += 16) {
-                    double e[16];
+                double e[16];  // as the hi chain: next 16 in flight
+                if (cnt >= 16) {
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) e[u] = eb[k + u];
+                    for (int u = 0; u < 16; ++u) e[u] = eb[u];
+                }
+                for (; k + 16 <= cnt; k += 16) {
+                    double f[16];  // (past the end: E's next buffer or L, unused)
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) f[u] = eb[k + 16 + u];
 #pragma unroll
                     for (int u = 0; u < 16; ++u) {
                         const double l = lo;
@@ -1145,14 +1221,23 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
                     }
 #pragma unroll
                     for (int u = 0; u < 16; ++u) lb[k + u] = e[u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) e[u] = f[u];
                 }
                 for (; k < cnt; ++k) {
                     lb[k] = lo;
                     lo = lo + eb[k];
                 }
             }
-        } else {
+        } else if (warp == 4) {  // (warps beyond 4, if any, only keep the barriers)
             const int c = it - 3;
+            if (done && c >= 1 && c - 1 < nch) {  // chunk c-1, stored a step ago -> its flag
+                __threadfence();
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;"
+                                 ::"l"(k2_flag(done, heavy, nb_flags, c - 1)), "r"(1u) : "memory");
+            }
             if (c >= 0 && c < nch) {
                 const int cnt = cnt_of(c);
                 const double* lb = L + (c % 2) * K2W_S;
@@ -1161,10 +1246,269 @@ k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, doub
                     out[k] = h_at(c, k) + lb[k];  // carry[b] = acc.value(), parallel.hpp:116-121
             }
         }
-        if (warp == 0) cp_async_wait<0>();
+        if (warp == 0) cp_async_wait<D - 1>();  // chunk it + 1 landed
         __syncthreads();
     }
 }
+
+__global__ void __launch_bounds__(160)
+k_scan_carry_split(const DevScalars* sc, const double* __restrict__ totals, double* carries,
+                   double* lpre, double* hpre) {
+    extern __shared__ __align__(16) double k2w[];
+    carry_chain<K2W_S>(blockIdx.x == 1, k2w, sc, totals, carries, lpre, hpre, nullptr, 0);
+}
+
+// ---------------------------------------------------------------------------
+// K2a / K2c, bulk-copy form (large tables, CompSumPos; the default): a warp
+// owns 32 consecutive blocks, one lane each, as before, but each lane's next
+// 128 elements (1 KB, contiguous in its block) arrive by one cp.async.bulk
+// that the lane issues itself, counted on a per-warp mbarrier, two chunks in
+// flight.  The smem-staged form moves 256 B per row per step with one chunk
+// in flight, so a warp's 32 blocks take ~0.22 ms however few warps compete
+// (measured inside the fused kernel) -- a whole-list wave; here a warp
+// streams 32 KB per step and finishes its 32 blocks in tens of microseconds,
+// so three warps per SM saturate HBM and the units are short.  Rows are 130
+// doubles apart: 16-B aligned for the bulk copy, and lanes r and r + 8 k read
+// different 16-B bank groups, so the LDS.128 reads take the minimum 4
+// wavefronts.  Same additions in the same order: bit-identical outputs.
+#ifndef KB_C_DEF
+#define KB_C_DEF 96
+#endif
+#ifndef KB_NB_DEF
+#define KB_NB_DEF 2
+#endif
+#ifndef KB_WARPS_DEF
+#define KB_WARPS_DEF 4
+#endif
+constexpr int KB_C = KB_C_DEF;          // elements per row chunk
+constexpr int KB_RS = KB_C + 2;         // row stride (doubles)
+constexpr int KB_NB = KB_NB_DEF;        // chunk buffers per warp
+constexpr int KB_WARPS = KB_WARPS_DEF;  // bulk-form warps per CTA (200 KB of rows)
+static_assert(KB_C % 32 == 0, "whole 32-element checkpoint pairs per chunk");
+struct __align__(128) KBWarp {
+    double tile[KB_NB][32][KB_RS];
+    uint64_t bar[KB_NB];
+};
+__device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"((unsigned)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// mbarriers of a warp's buffers (count 1: lane 0's arrive.expect_tx)
+__device__ __forceinline__ void kb_init(KBWarp& W) {
+    if ((threadIdx.x & 31) == 0) {
+        for (int i = 0; i < KB_NB; ++i) mbar_init(&W.bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+}
+
+// One 32-block unit.  CK = false: block totals (pass 1, parallel.hpp:104-114);
+// CK = true: checkpoints from run.add(carry[b]) (pass 3 state, :122-127).
+// par: the buffers' mbarrier phase bits, carried across units.  flags
+// (fused launch only): wait for the chain's flag of the block's carry chunk.
+template <bool CK>
+__device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
+                                        const double* __restrict__ lw, const double* __restrict__ hw,
+                                        const DevScalars* sc, double* __restrict__ totals,
+                                        double2* __restrict__ lck, double2* __restrict__ hck,
+                                        const double* carries, const unsigned* flags,
+                                        uint64_t nb_flags) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nl = sc->nl, nh = sc->nh;
+    const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    // units alternate between the lists (light 0, heavy 0, light 1, ...):
+    // the two chains publish block j's carries at about the same time, so
+    // units taken in order follow both chains
+    const uint64_t nlu = (nbl + 31) / 32, nhu = (nbh + 31) / 32;
+    const uint64_t m = nlu < nhu ? nlu : nhu;
+    bool heavy;
+    uint64_t idx;
+    if (wu < 2 * m) {
+        heavy = wu & 1;
+        idx = wu >> 1;
+    } else {
+        heavy = nhu > nlu;
+        idx = wu - m;
+    }
+    const uint64_t j = idx * 32 + lane;  // block within its list
+    const double* src = nullptr;
+    double2* ck = nullptr;
+    int len = 0;
+    if (!heavy && j < nbl) {
+        src = lw + j * SCAN_BLOCK;
+        ck = lck + j * (SCAN_BLOCK / CK_STRIDE);
+        len = static_cast<int>(umin64(SCAN_BLOCK, nl - j * SCAN_BLOCK));
+    } else if (heavy && j < nbh) {
+        src = hw + j * SCAN_BLOCK;
+        ck = hck + j * (SCAN_BLOCK / CK_STRIDE);
+        len = static_cast<int>(umin64(SCAN_BLOCK, nh - j * SCAN_BLOCK));
+    }
+    const uint64_t b = heavy ? nbl + j : j;  // index into totals / carries
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    if (maxlen == 0) return;
+    const int nch = (maxlen + KB_C - 1) / KB_C;
+    auto issue = [&](int c) {
+        const int buf = c % KB_NB;
+        const int cnt = max(0, min(KB_C, len - c * KB_C));
+        const unsigned bytes = static_cast<unsigned>(cnt & ~1) * 8u;  // whole 16-B pairs
+        unsigned tot = bytes;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        // the buffer's last readers are done (__syncwarp in the caller); order
+        // their generic-proxy reads before the async-proxy writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0) mbar_expect(&W.bar[buf], tot);
+        if (bytes) bulk_g2s(&W.tile[buf][lane][0], src + c * KB_C, bytes, &W.bar[buf]);
+        if (cnt & 1) W.tile[buf][lane][cnt - 1] = __ldg(src + c * KB_C + cnt - 1);  // odd tail
+    };
+#pragma unroll
+    for (int c = 0; c < KB_NB; ++c)
+        if (c < nch) issue(c);
+    CompSumPos cs{0.0, 0.0};
+    if (CK && len > 0) {
+        double carry;
+        if (flags) {  // the chain CTA of this launch publishes the carries
+            const unsigned* f = k2_flag(flags, heavy, nb_flags, j / K2F_S);
+            // relaxed polls (an acquire per poll invalidates the SM's L1), one
+            // acquire fence once the flag is seen
+            while (*reinterpret_cast<const volatile unsigned*>(f) == 0) __nanosleep(128);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            carry = __ldcg(carries + b);
+        } else {
+            carry = __ldg(carries + b);
+        }
+        cs.add(carry);  // run.add(carry[b]) = (carry, 0), parallel.hpp:124
+    }
+    for (int c = 0; c < nch; ++c) {
+        const int buf = c % KB_NB;
+        while (!mbar_try(&W.bar[buf], (par >> buf) & 1u)) {
+        }
+        par ^= 1u << buf;
+        const int cnt = min(KB_C, len - c * KB_C);
+        if (cnt == KB_C) {
+            const double2* row = reinterpret_cast<const double2*>(&W.tile[buf][lane][0]);
+#pragma unroll 1
+            for (int q = 0; q < KB_C / 32; ++q) {
+                double2 k0, k1;
+                k0 = make_double2(cs.hi, cs.lo);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const double2 v = row[q * 16 + e];
+                    cs.add(v.x);
+                    cs.add(v.y);
+                }
+                k1 = make_double2(cs.hi, cs.lo);
+#pragma unroll
+                for (int e = 8; e < 16; ++e) {
+                    const double2 v = row[q * 16 + e];
+                    cs.add(v.x);
+                    cs.add(v.y);
+                }
+                if (CK) {
+                    double2* d = ck + (c * KB_C + q * 32) / CK_STRIDE;
+                    __stcs(d, k0);
+                    __stcs(d + 1, k1);
+                }
+            }
+        } else if (cnt > 0) {
+            const double* row = &W.tile[buf][lane][0];
+            for (int q = 0; q * 32 < cnt; ++q) {  // 32-element sub-chunks, as k_scan_blocks_ckpt
+                const int n32 = min(32, cnt - q * 32);
+                double2 k0 = make_double2(cs.hi, cs.lo), k1 = k0;
+                for (int e = 0; e < n32; ++e) {
+                    if (e == CK_STRIDE) k1 = make_double2(cs.hi, cs.lo);
+                    cs.add(row[q * 32 + e]);
+                }
+                if (CK) {
+                    double2* d = ck + (c * KB_C + q * 32) / CK_STRIDE;
+                    __stcs(d, k0);
+                    __stcs(d + 1, k1);
+                }
+            }
+        }
+        __syncwarp();
+        if (c + KB_NB < nch) issue(c + KB_NB);
+    }
+    if (!CK && len > 0) totals[b] = cs.value();  // carry[b] = local.value(), parallel.hpp:114
+}
+
+// K2a, bulk form: warp units in a grid stride.
+__global__ void __launch_bounds__(KB_WARPS * 32, 1)
+k_totals_kb(const double* __restrict__ lw, const double* __restrict__ hw, const DevScalars* sc,
+            double* __restrict__ totals, uint32_t wunits) {
+    extern __shared__ __align__(128) unsigned char kbs[];
+    KBWarp& W = reinterpret_cast<KBWarp*>(kbs)[threadIdx.x >> 5];
+    kb_init(W);
+    unsigned par = 0;
+    for (uint32_t wu = blockIdx.x * KB_WARPS + (threadIdx.x >> 5); wu < wunits;
+         wu += gridDim.x * KB_WARPS)
+        kb_unit<false>(wu, W, par, lw, hw, sc, totals, nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+// K2c, bulk form, after a separate K2b (WRS_B200_K2_FUSE=0).
+__global__ void __launch_bounds__(KB_WARPS * 32, 1)
+k_ckpt_kb(const double* __restrict__ lw, const double* __restrict__ hw, double2* __restrict__ lck,
+          double2* __restrict__ hck, const DevScalars* sc, const double* __restrict__ carries,
+          uint32_t wunits) {
+    extern __shared__ __align__(128) unsigned char kbs[];
+    KBWarp& W = reinterpret_cast<KBWarp*>(kbs)[threadIdx.x >> 5];
+    kb_init(W);
+    unsigned par = 0;
+    for (uint32_t wu = blockIdx.x * KB_WARPS + (threadIdx.x >> 5); wu < wunits;
+         wu += gridDim.x * KB_WARPS)
+        kb_unit<true>(wu, W, par, lw, hw, sc, nullptr, lck, hck, carries, nullptr, 0);
+}
+constexpr int KB_SMEM = KB_WARPS * static_cast<int>(sizeof(KBWarp));
+
+// K2b and K2c fused (the checkpoint form): the chain is one dependent FP64
+// add per block total -- ~0.16 ms at n = 1e8 on two CTAs while the other SMs
+// idle -- so the checkpoint units run concurrently and start each block as
+// soon as the chain has published its carry chunk.  CTAs take roles from a
+// ticket in the order they start: tickets 0 and 1 run the light / heavy
+// chains, every other CTA's warps take 32-block units in order from a
+// counter.  A CTA waits only on chain CTAs that already hold their tickets,
+// so they are resident and the waits end.
+constexpr int K2F_D = 4, K2F_RX = 6;  // chain prefetch depth / x ring (loaded L2 latency)
+// one CTA per SM (the bulk rows fill shared memory), so the chain CTAs have
+// their SMs to themselves
+constexpr int K2F_SMEM = KB_SMEM > k2w_smem(K2F_S, K2F_RX) ? KB_SMEM : k2w_smem(K2F_S, K2F_RX);
+constexpr int K2F_THREADS = 32 * (KB_WARPS > 5 ? KB_WARPS : 5);  // chain: 5 warps
+__global__ void __launch_bounds__(K2F_THREADS, 1)
+k_carry_ckpt(DevScalars* sc, const double* __restrict__ totals, double* carries, double* lpre,
+             double* hpre, const double* __restrict__ lw, const double* __restrict__ hw,
+             double2* __restrict__ lck, double2* __restrict__ hck, unsigned* flags,
+             uint64_t nb_flags, uint32_t wunits) {
+    extern __shared__ __align__(128) double k2f[];
+    __shared__ unsigned role;
+    if (threadIdx.x == 0) role = atomicAdd(&sc->k2_ticket, 1u);
+    __syncthreads();
+    const unsigned t = role;
+    if (t < 2) {
+        carry_chain<K2F_S, K2F_D, K2F_RX>(t == 1, k2f, sc, totals, carries, lpre, hpre, flags,
+                                          nb_flags);
+        return;
+    }
+    const int wq = threadIdx.x >> 5;
+    if (wq >= KB_WARPS) return;
+    KBWarp& W = reinterpret_cast<KBWarp*>(k2f)[wq];
+    kb_init(W);
+    unsigned par = 0;
+    const int lane = threadIdx.x & 31;
+    for (;;) {  // units in order: the earliest carries are published first
+        unsigned wu = 0;
+        if (lane == 0) wu = atomicAdd(&sc->k2_work, 1u);
+        wu = __shfl_sync(0xffffffffu, wu, 0);
+        if (wu >= wunits) break;
+        kb_unit<true>(wu, W, par, lw, hw, sc, nullptr, lck, hck, carries, flags, nb_flags);
+    }
+}
+
 
 template <class CS>
 __global__ void __launch_bounds__(32)
@@ -1783,6 +2127,7 @@ cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate
     A(ws.split_h, P + 1);
     A(ws.split_s, P + 1);
     A(ws.sc, 1);
+    A(ws.k2_flags, k2_flag_words(n));
     if (separate_outputs) {
         A(ws.lrank_own, n);
         A(ws.hshare_own, n);
@@ -1812,7 +2157,7 @@ void workspace_free(Workspace& ws) {
     void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.hidx,       ws.lw,
                     ws.hw,       ws.lpre,     ws.hpre,        ws.totals,
                     ws.carries,  ws.split_l,  ws.split_h,     ws.split_s,    ws.sc,
-                    ws.lrank_own, ws.hshare_own, ws.lck,       ws.hck};
+                    ws.lrank_own, ws.hshare_own, ws.lck,       ws.hck,    ws.k2_flags};
     for (void* p : ptrs)
         if (p) dev_free(p);
     ws = Workspace{};
@@ -1885,6 +2230,25 @@ static bool k2_ckpt_enabled() {
     return !(e && e[0] == '0');
 }
 
+static int sm_count_psa() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Bulk-copy K2a / K2c (WRS_B200_K2_KB=0: the smem-staged kernels).
+static bool k2_kb_enabled() {
+    const char* e = std::getenv("WRS_B200_K2_KB");
+    return !(e && e[0] == '0');
+}
+
+// K2b fused with the checkpoint pass (WRS_B200_K2_FUSE=0: two kernels).
+static bool k2_fuse_enabled() {
+    const char* e = std::getenv("WRS_B200_K2_FUSE");
+    return !(e && e[0] == '0');
+}
+
 cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
                              Bucket* d_b, Workspace& ws, cudaStream_t st, cudaEvent_t* ev) {
     const int k1_smem = K1_TILE * 10;
@@ -1901,6 +2265,9 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     cudaFuncSetAttribute(k_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
     cudaFuncSetAttribute(k_pack<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k4_smem);
     cudaFuncSetAttribute(k_scan_carry_split, cudaFuncAttributeMaxDynamicSharedMemorySize, K2W_SMEM);
+    cudaFuncSetAttribute(k_carry_ckpt, cudaFuncAttributeMaxDynamicSharedMemorySize, K2F_SMEM);
+    cudaFuncSetAttribute(k_totals_kb, cudaFuncAttributeMaxDynamicSharedMemorySize, KB_SMEM);
+    cudaFuncSetAttribute(k_ckpt_kb, cudaFuncAttributeMaxDynamicSharedMemorySize, KB_SMEM);
     cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, K4B_SMEM);
     const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
     const uint64_t nblocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1;  // light + heavy blocks
@@ -1964,24 +2331,49 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
             k_scan_blocks<PASS3, CompSum><<<k2_grid, K2_WARPS * 32, 0, st>>>(                     \
                 ws.lw, ws.hw, ws.lpre, ws.hpre, ws.sc, ws.totals, ws.carries);                    \
     } while (0)
+    // large tables: the bulk-copy forms of K2a / K2c (WRS_B200_K2_KB=0: the
+    // smem-staged forms)
+    const bool kb = pos && !split && !direct && k2_kb_enabled();
+    const int sms = sm_count_psa();
+    // per-list units: nlu + nhu <= (blocks + 31) / 32 + 1 (empty ones return at once)
+    const uint32_t kb_units = static_cast<uint32_t>((nblocks + 31) / 32 + 1);
+    const unsigned kb_grid = static_cast<unsigned>(
+        std::min<uint64_t>((kb_units + KB_WARPS - 1) / KB_WARPS, sms));
     if (pos && !split && !direct && std::getenv("WRS_B200_K2_BULK"))
         k_scan_totals_bulk<CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.sc,
                                                                           ws.totals);
+    else if (kb)
+        k_totals_kb<<<kb_grid, KB_WARPS * 32, KB_SMEM, st>>>(ws.lw, ws.hw, ws.sc, ws.totals, kb_units);
     else
         K2_LAUNCH(false);
     REC(2);
-    if (pos)
-        k_scan_carry_split<<<2, 160, K2W_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
-    else
-        k_scan_carry<CompSum><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
-    REC(3);
     // large tables: checkpoints instead of full prefix arrays (1 B per item
     // written instead of 8; K3 recomputes what it probes)
     ws.ckpt = pos && !split && !direct && k2_ckpt_enabled();
-    if (ws.ckpt)
+    // ... and the carry chain fused with them (WRS_B200_K2_FUSE=0: separate)
+    const bool fuse = ws.ckpt && kb && k2_fuse_enabled();
+    if (fuse) {
+        // one CTA per SM: two chains, the rest checkpoint units
+        const unsigned grid = static_cast<unsigned>(
+            std::min<uint64_t>(2 + (kb_units + KB_WARPS - 1) / KB_WARPS, sms));
+        e = cudaMemsetAsync(ws.k2_flags, 0, k2_flag_words(ws.n) * 4, st);
+        if (e != cudaSuccess) return e;
+        k_carry_ckpt<<<grid, K2F_THREADS, K2F_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre,
+                                                  ws.lw, ws.hw, ws.lck, ws.hck, ws.k2_flags,
+                                                  k2_flag_slots(ws.n), kb_units);
+    } else if (pos) {
+        k_scan_carry_split<<<2, 160, K2W_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
+    } else {
+        k_scan_carry<CompSum><<<2, 32, 0, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
+    }
+    REC(3);  // (fused: K2c ran inside the launch above, so its stage time is ~0)
+    if (!fuse && ws.ckpt && kb)
+        k_ckpt_kb<<<kb_grid, KB_WARPS * 32, KB_SMEM, st>>>(ws.lw, ws.hw, ws.lck, ws.hck, ws.sc,
+                                                          ws.carries, kb_units);
+    else if (!fuse && ws.ckpt)
         k_scan_blocks_ckpt<<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.lck, ws.hck, ws.sc,
                                                               ws.carries);
-    else
+    else if (!fuse)
         K2_LAUNCH(true);
 #undef K2_LAUNCH
     REC(4);

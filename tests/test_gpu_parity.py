@@ -122,13 +122,16 @@ def check_checkpoints(ck, prefix, x):
         assert val[live].tobytes() == prefix[pos[live] + 1].tobytes(), e
 
 @pytest.mark.parametrize("k2", ["split", "direct", "direct-lpw1", "direct-lpw32", "staged",
-                                "staged-k1staged", "staged-k2bulk"])
+                                "staged-k1staged", "staged-k2bulk", "staged-nofuse"])
 def test_stages_bit_exact(P, k2, monkeypatch):
     if k2.endswith("k1staged"):  # K1's staged form (the unstaged one is the default)
         monkeypatch.setenv("WRS_B200_K1", "staged")
         k2 = k2.split("-")[0]
     if k2.endswith("k2bulk"):  # K2a through TMA bulk copies (measured slower, opt-in)
         monkeypatch.setenv("WRS_B200_K2_BULK", "1")
+        k2 = k2.split("-")[0]
+    if k2.endswith("nofuse"):  # K2b and the checkpoint pass as two kernels
+        monkeypatch.setenv("WRS_B200_K2_FUSE", "0")
         k2 = k2.split("-")[0]
     # K2a/K2c have three forms (chains split over warps for a few blocks,
     # register-direct for small tables with 1..32 chains per warp, and
