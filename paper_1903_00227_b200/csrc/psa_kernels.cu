@@ -592,7 +592,10 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 // Fused K2b+K2c publication flags: per list, one word per chunk of K2F_S
 // carries, each on its own 128-B line so the waiting warps poll many lines
 // rather than one.  nb_flags = chunk slots per list.
-constexpr int K2F_S = 256;  // totals per chain chunk (publication granularity)
+#ifndef K2F_S_DEF
+#define K2F_S_DEF 512
+#endif
+constexpr int K2F_S = K2F_S_DEF;  // totals per chain chunk (publication granularity)
 __host__ __device__ inline uint64_t k2_flag_slots(uint64_t n) {
     return ((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 2 + K2F_S - 1) / K2F_S + 1;
 }

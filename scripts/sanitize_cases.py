@@ -43,11 +43,18 @@ def main():
              np.full(777, 0.5), np.concatenate([[1e6], np.ones(4999)]),
              np.where(rng.random(9000) < 0.5, 1.0, rng.random(9000) + 0.5),
              np.array([1e300, 2e300, 3e300, 1.0])]
-    forms = {"split": ("9223372036854775807", "9223372036854775807"),
-             "direct": ("0", "9223372036854775807"), "staged": ("0", "0")}
-    for form, (smax, dmax) in forms.items():
+    big = "9223372036854775807"
+    # staged = the large-table forms: bulk-copy K2a + fused K2b/K2c (default),
+    # bulk-copy with a separate K2b, and the smem-staged kernels
+    forms = {"split": (big, big, {}), "direct": ("0", big, {}), "staged": ("0", "0", {}),
+             "staged-nofuse": ("0", "0", {"WRS_B200_K2_FUSE": "0"}),
+             "staged-nokb": ("0", "0", {"WRS_B200_K2_KB": "0"})}
+    for form, (smax, dmax, extra) in forms.items():
         os.environ["WRS_B200_K2_SPLIT_MAX"] = smax
         os.environ["WRS_B200_K2_DIRECT_MAX"] = dmax
+        for e in ("WRS_B200_K2_FUSE", "WRS_B200_K2_KB"):
+            os.environ.pop(e, None)
+        os.environ.update(extra)
         for w in cases:
             for P in (1, 7, wrs.default_jobs(w.size), w.size + 3):
                 W = wrs.Weights.from_array(w)
@@ -56,8 +63,8 @@ def main():
                 S.free()
                 W.free()
         print("build", form, "ok", flush=True)
-    for k in ("WRS_B200_K2_SPLIT_MAX", "WRS_B200_K2_DIRECT_MAX"):
-        os.environ.pop(k)
+    for k in ("WRS_B200_K2_SPLIT_MAX", "WRS_B200_K2_DIRECT_MAX", "WRS_B200_K2_FUSE", "WRS_B200_K2_KB"):
+        os.environ.pop(k, None)
 
     # draws: direct plan, then the region plan forced on 2^16-bucket regions
     w = port.generate_powerlaw(300_007, 0.5, 9)

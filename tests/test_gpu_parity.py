@@ -122,7 +122,8 @@ def check_checkpoints(ck, prefix, x):
         assert val[live].tobytes() == prefix[pos[live] + 1].tobytes(), e
 
 @pytest.mark.parametrize("k2", ["split", "direct", "direct-lpw1", "direct-lpw32", "staged",
-                                "staged-k1staged", "staged-k2bulk", "staged-nofuse"])
+                                "staged-k1staged", "staged-k2bulk", "staged-nofuse",
+                                "staged-nokb"])
 def test_stages_bit_exact(P, k2, monkeypatch):
     if k2.endswith("k1staged"):  # K1's staged form (the unstaged one is the default)
         monkeypatch.setenv("WRS_B200_K1", "staged")
@@ -133,9 +134,13 @@ def test_stages_bit_exact(P, k2, monkeypatch):
     if k2.endswith("nofuse"):  # K2b and the checkpoint pass as two kernels
         monkeypatch.setenv("WRS_B200_K2_FUSE", "0")
         k2 = k2.split("-")[0]
+    if k2.endswith("nokb"):  # the smem-staged K2a / K2c instead of the bulk-copy forms
+        monkeypatch.setenv("WRS_B200_K2_KB", "0")
+        k2 = k2.split("-")[0]
     # K2a/K2c have three forms (chains split over warps for a few blocks,
-    # register-direct for small tables with 1..32 chains per warp, and
-    # smem-staged above 2^25 items); all must produce the same prefix arrays
+    # register-direct for small tables with 1..32 chains per warp, and the
+    # large-table form above 2^25 items: bulk-copy rows with K2b fused into
+    # the checkpoint pass); all must produce the same prefix arrays
     monkeypatch.setenv("WRS_B200_K2_SPLIT_MAX", str(2**62 if k2 == "split" else 0))
     monkeypatch.setenv("WRS_B200_K2_DIRECT_MAX", str(0 if k2 == "staged" else 2**62))
     if "lpw" in k2:
