@@ -11,5 +11,5 @@ timeout 600 $CMD > gpurun_out/plain_${TAG}.log 2>&1; echo plain_rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo ncu1_rc=$?
 timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_region|k_pack|k_assemble|k_partition|k_scan|k_split" -s 0 -c 19 \
+    -k regex:"k_region|k_pack|k_assemble|k_partition|k_scan|k_split|k_totals|k_carry|k_ckpt" -s 0 -c 19 \
     -o gpurun_out/prof_${TAG} $CMD > gpurun_out/ncu_full_${TAG}.log 2>&1; echo ncu2_rc=$?
