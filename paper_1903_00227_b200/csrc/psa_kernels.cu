@@ -206,16 +206,32 @@ struct TileCells {
 
 // Loads the tile's weights into xs (when KEEP), fills cells (ballots, offsets,
 // totals).  Ends with __syncthreads().
+// classify_cells: the same from weights already in registers (xs[r] = item
+// base + r * K1_THREADS + tid).
+__device__ __forceinline__ void classify_cells(const double* xs, uint64_t n, uint64_t base,
+                                               double wn, TileCells& C);
 template <bool KEEP>
 __device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint64_t n,
                                               uint64_t base, double wn, double* xs,
                                               TileCells& C) {
+    const int tid = threadIdx.x;
+    double x[K1_ROWS];
+#pragma unroll
+    for (int r = 0; r < K1_ROWS; ++r) {
+        const uint64_t gi = base + r * K1_THREADS + tid;
+        x[r] = gi < n ? __ldg(w + gi) : 0.0;
+        if (KEEP) xs[r] = x[r];
+    }
+    classify_cells(x, n, base, wn, C);
+}
+
+__device__ __forceinline__ void classify_cells(const double* xs, uint64_t n, uint64_t base,
+                                               double wn, TileCells& C) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int r = 0; r < K1_ROWS; ++r) {
         const uint64_t gi = base + r * K1_THREADS + tid;
-        const double x = gi < n ? __ldg(w + gi) : 0.0;
-        if (KEEP) xs[r] = x;
+        const double x = xs[r];
         const bool valid = gi < n;
         const bool light = valid && x <= wn;  // ties are light (alias.hpp:60)
         const unsigned lm = __ballot_sync(0xffffffffu, light);
@@ -259,6 +275,69 @@ __device__ __forceinline__ void classify_tile(const double* __restrict__ w, uint
         }
     }
     __syncthreads();
+}
+
+#ifndef K1_LOOKBACK_WIN
+#define K1_LOOKBACK_WIN 1  // look-back windows of 32 tiles per round (measured: 2, 4, 8 are slower)
+#endif
+// Decoupled look-back (warp 0 of the tile's CTA): publishes the tile's light
+// count, sums predecessors' counts back to the first inclusive prefix, then
+// publishes its own inclusive prefix; s_excl = lights before the tile.
+__device__ __forceinline__ void k1_lookback(uint64_t tile, uint64_t ntiles, uint64_t n,
+                                            uint32_t totL, unsigned long long* status,
+                                            DevScalars* sc, unsigned long long& s_excl) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+        if (lane == 0) st_volatile(&status[0], FLAG_P | totL);
+    } else {
+        if (lane == 0) st_volatile(&status[tile], FLAG_A | totL);
+        // 128 predecessors per round (4 per lane): with hundreds of tiles
+        // in flight the inclusive prefixes lag far behind, and a round is
+        // one memory latency
+        constexpr int LB = K1_LOOKBACK_WIN;
+        long long p = static_cast<long long>(tile) - 1;
+        while (true) {
+            unsigned long long v[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const long long idx = p - (u * 32 + lane);
+                v[u] = FLAG_P;
+                if (idx >= 0) v[u] = ld_volatile(&status[idx]);
+            }
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const long long idx = p - (u * 32 + lane);
+                while ((v[u] >> 62) == 0) v[u] = ld_volatile(&status[idx]);
+            }
+            bool done = false;
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                if (!done) {
+                    const unsigned pm = __ballot_sync(0xffffffffu, (v[u] >> 62) == 2);
+                    unsigned long long c = v[u] & VAL_MASK;
+                    if (pm) {
+                        const int first = __ffs(pm) - 1;
+                        if (lane > first) c = 0;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                    excl += c;
+                    done = pm != 0;
+                }
+            }
+            if (done) break;
+            p -= 32 * LB;
+        }
+        if (lane == 0) st_volatile(&status[tile], FLAG_P | (excl + totL));
+    }
+    if (lane == 0) {
+        s_excl = excl;
+        if (tile + 1 == ntiles) {
+            sc->nl = excl + totL;
+            sc->nh = n - (excl + totL);
+        }
+    }
 }
 
 // ===========================================================================
@@ -364,9 +443,6 @@ k_partition(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalar
 #ifndef K1D_MINB
 #define K1D_MINB 5
 #endif
-#ifndef K1_LOOKBACK_WIN
-#define K1_LOOKBACK_WIN 1  // look-back windows of 32 tiles per round (measured: 2, 4, 8 are slower)
-#endif
 __global__ void __launch_bounds__(K1_THREADS, K1D_MINB)
 k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, DevScalars* sc,
                    unsigned long long* status, double* __restrict__ lw, uint32_t* __restrict__ hidx,
@@ -381,61 +457,7 @@ k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, De
     const uint64_t base = tile * K1_TILE;
     double xs[K1_ROWS];
     classify_tile<true>(w, n, base, __ldcg(&sc->wn), xs, C);
-    if (warp == 0) {
-        const uint32_t totL = C.totL;
-        // decoupled look-back for the number of lights before this tile
-        unsigned long long excl = 0;
-        if (tile == 0) {
-            if (lane == 0) st_volatile(&status[0], FLAG_P | totL);
-        } else {
-            if (lane == 0) st_volatile(&status[tile], FLAG_A | totL);
-            // 128 predecessors per round (4 per lane): with hundreds of tiles
-            // in flight the inclusive prefixes lag far behind, and a round is
-            // one memory latency
-            constexpr int LB = K1_LOOKBACK_WIN;
-            long long p = static_cast<long long>(tile) - 1;
-            while (true) {
-                unsigned long long v[LB];
-#pragma unroll
-                for (int u = 0; u < LB; ++u) {
-                    const long long idx = p - (u * 32 + lane);
-                    v[u] = FLAG_P;
-                    if (idx >= 0) v[u] = ld_volatile(&status[idx]);
-                }
-#pragma unroll
-                for (int u = 0; u < LB; ++u) {
-                    const long long idx = p - (u * 32 + lane);
-                    while ((v[u] >> 62) == 0) v[u] = ld_volatile(&status[idx]);
-                }
-                bool done = false;
-#pragma unroll
-                for (int u = 0; u < LB; ++u) {
-                    if (!done) {
-                        const unsigned pm = __ballot_sync(0xffffffffu, (v[u] >> 62) == 2);
-                        unsigned long long c = v[u] & VAL_MASK;
-                        if (pm) {
-                            const int first = __ffs(pm) - 1;
-                            if (lane > first) c = 0;
-                        }
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-                        excl += c;
-                        done = pm != 0;
-                    }
-                }
-                if (done) break;
-                p -= 32 * LB;
-            }
-            if (lane == 0) st_volatile(&status[tile], FLAG_P | (excl + totL));
-        }
-        if (lane == 0) {
-            s_excl = excl;
-            if (tile + 1 == ntiles) {
-                sc->nl = excl + totL;
-                sc->nh = n - (excl + totL);
-            }
-        }
-    }
+    if (warp == 0) k1_lookback(tile, ntiles, n, C.totL, status, sc, s_excl);
     __syncthreads();
     const uint64_t L0 = s_excl, H0 = base - s_excl;
     const unsigned lt = lanemask_lt();
@@ -453,6 +475,7 @@ k_partition_direct(const double* __restrict__ w, uint64_t n, uint64_t ntiles, De
         }
     }
 }
+
 
 // ===========================================================================
 // K2a / K2c: per-2048-block Neumaier chains, one lane per block
