@@ -279,10 +279,11 @@ struct RegionGeom {
     uint32_t ov_cap;   // records in the overflow slab (after the nreg slabs)
 };
 
-// per (tile, region): global start of the tile's run and its tile-local start
+// per (tile, region): slab position of the tile's run and the END of its
+// padded slots in the tile's stage (the run starts where the previous ends)
 struct RunInfo {
     uint32_t goff;
-    uint32_t loc;
+    uint32_t end;
 };
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -326,9 +327,19 @@ __device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t 
 // written to its slab as one contiguous block.  The tile slot of every draw
 // is recorded (q order) for RD, so the (non-deterministic) order inside a run
 // never needs to be reproduced.
+// Runs are padded to whole groups of RUN_ALIGN records (slab and stage
+// positions stay multiples of 4: 32-B aligned records, 16-B aligned results),
+// so RB writes each run with one bulk copy and RD stages results with 16-B
+// copies; a padding slot holds a record whose draw index is REC_PAD, which
+// RC and the counting pass skip.
+constexpr uint32_t RUN_ALIGN = 4;
+constexpr uint32_t REC_PAD = 0xffffffffu;  // (draw indices within a chunk are < 2^31)
+__host__ __device__ inline uint32_t stage_slots(uint32_t nreg, uint32_t tile) {
+    return tile + (RUN_ALIGN - 1) * nreg;
+}
 __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t tile) {
     const size_t head = (4 * static_cast<size_t>(nreg) + 2) * 4;
-    return ((head + 15) & ~size_t(15)) + tile * sizeof(uint2);
+    return ((head + 15) & ~size_t(15)) + stage_slots(nreg, tile) * sizeof(uint2);
 }
 
 // ORDER = false (aggregated draws): the answers are only counted, never put
@@ -365,8 +376,8 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     uint32_t* cnt = reinterpret_cast<uint32_t*>(rs_smem);  // [nreg] draws per region
     uint32_t* start = cnt + nreg;                          // [nreg + 1] run starts in the stage
     uint32_t* fill = start + nreg + 1;                     // [nreg] fill cursors
-    uint32_t* goff = fill + nreg;                          // [nreg] slab base, then slab - stage offset
-    uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((4 * nreg + 2) * 4 + 15) & ~15u));
+    uint32_t* goff = fill + nreg;                          // [nreg] the runs' slab positions
+    uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((4 * nreg + 2) * 4 + 15) & ~15u));  // padded runs
     const uint64_t tile = static_cast<uint64_t>(tile0) + blockIdx.x;
     const uint64_t tbase = tile * (TT * RS_ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -415,7 +426,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         uint32_t carry = 0;
         for (uint32_t r0 = 0; r0 < nreg; r0 += 32) {
             const uint32_t reg = r0 + lane;
-            const uint32_t c = reg < nreg ? cnt[reg] : 0;
+            const uint32_t c = reg < nreg ? (cnt[reg] + RUN_ALIGN - 1) & ~(RUN_ALIGN - 1) : 0;
             uint32_t x = c;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -431,7 +442,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         if (lane == 0) start[nreg] = carry;
     } else {  // claim slab space for each non-empty run of this tile
         for (uint32_t reg = threadIdx.x - 32; reg < nreg; reg += TT - 32) {
-            const uint32_t c = cnt[reg];
+            const uint32_t c = (cnt[reg] + RUN_ALIGN - 1) & ~(RUN_ALIGN - 1);  // padded run
             uint32_t g = 0;
             if (c) {
                 const uint32_t base = atomicAdd(&cursor[reg], c);
@@ -450,6 +461,13 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         }
     }
     __syncthreads();
+    // run table and padding records (slots [start + cnt, next start), disjoint
+    // from the slots the draws take below)
+    for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
+        if (ORDER) runs[tile * nreg + reg] = RunInfo{goff[reg], start[reg + 1]};
+        for (uint32_t i = start[reg] + cnt[reg]; i < start[reg + 1]; ++i)
+            stage[i] = make_uint2(REC_PAD, 0u);
+    }
     const uint32_t t32 = static_cast<uint32_t>(tbase);
 #pragma unroll
     for (int r = 0; r < RS_ROWS; ++r) {
@@ -460,30 +478,30 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
             if (ORDER) slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
     }
-    for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
-        const uint32_t g = goff[reg];
-        goff[reg] = g - start[reg];  // slab position of staged slot i = goff[region] + i
-        if (ORDER) runs[tile * nreg + reg] = RunInfo{g, start[reg]};
-    }
-    __syncthreads();
     // (no early exit on overflow: an overflowed run is written to the start
     // of the overflow slab, which stays in bounds, and RD recomputes the whole
     // chunk directly whenever the flag is set)
-    // staged tile -> slabs: slot i goes to goff[region of its bucket] + i, so
-    // consecutive slots of a run land on consecutive slab positions (one flat,
-    // fully unrolled pass; no per-run loop)
+    // staged tile -> slabs: one bulk copy per run (32-B aligned on both
+    // sides, whole 32-B groups), issued by the run's thread once every
+    // thread's generic-proxy stage writes are ordered before the async proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
     const uint64_t pol = policy_evict_first();
-#pragma unroll
-    for (int r = 0; r < RS_ROWS; ++r) {
-        const uint32_t i = r * TT + threadIdx.x;
-        if (i < kc_left) {
-            const uint2 v = stage[i];
-            WRS_CHECK(v.y < n32 && goff[v.y >> rg.shift] + i <
-                                          static_cast<uint64_t>(rg.nreg) * rg.cap + rg.ov_cap);
-            uint2* dst = rec + (goff[v.y >> rg.shift] + i);
-            asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
-                         :: "l"(dst), "r"(v.x), "r"(v.y), "l"(pol));
+    bool issued = false;
+    for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
+        const uint32_t len = start[reg + 1] - start[reg];
+        if (len) {
+            WRS_CHECK(goff[reg] % RUN_ALIGN == 0 &&
+                      goff[reg] + len <= static_cast<uint64_t>(rg.nreg) * rg.cap + rg.ov_cap);
+            const unsigned src = static_cast<unsigned>(__cvta_generic_to_shared(stage + start[reg]));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                         :: "l"(rec + goff[reg]), "r"(src), "r"(len * 8u), "l"(pol) : "memory");
+            issued = true;
         }
+    }
+    if (issued) {  // the stage must stay intact until the copies have read it
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
 }
 
@@ -521,20 +539,22 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
-        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
+        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(REC_PAD, 0);
     }
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u)
         WRS_CHECK(p0 + u * 256 + threadIdx.x >= valid_end || r[u].y < rg.g.n);
     // bucket gathers as LDGSTS into shared memory: measured 232 G random
     // L2-resident 16-B rows/s vs 200 G for LDG (scripts/microbench/
-    // l2_gather_bench.cu); each thread reads back only its own rows
+    // l2_gather_bench.cu); each thread reads back only its own rows.
+    // Padding records (REC_PAD) are skipped.
     __shared__ uint4 bk_s[RC_ROWS * 256];
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
-                     ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
+        if (r[u].x != REC_PAD)
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
+                         ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -542,7 +562,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
-        if (p < valid_end) {
+        if (p < valid_end && r[u].x != REC_PAD) {
             double x;
             if (W1) {
                 if constexpr (PHX)
@@ -571,7 +591,7 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
                    const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
                    const uint16_t* __restrict__ slot_of, const uint32_t* __restrict__ res,
                    uint32_t out_base, uint32_t* __restrict__ out) {
-    extern __shared__ __align__(16) uint32_t stage[];  // (TT * RS_ROWS) results
+    extern __shared__ __align__(16) uint32_t stage[];  // stage_slots() results (padded runs)
     const uint64_t tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t tbase = tile * (TT * RS_ROWS);
@@ -604,10 +624,11 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         for (int i = 0; i < VP; ++i)
             sv[i] = *reinterpret_cast<const uint2*>(slot_of + tbase + (i * TT + threadIdx.x) * 4);
     }
-    // this tile's runs -> shared memory with LDGSTS: no register staging, so
-    // every element of the tile is in flight at once.  Warp w owns runs w,
-    // w + WARPS, ...; their descriptors are loaded by one lane each, all at
-    // once, and handed round by shuffles (no load latency per run).
+    // this tile's runs -> shared memory with 16-B LDGSTS (runs are padded to
+    // 4 results, 16-B aligned in the slab and the stage): no register
+    // staging, so every element of the tile is in flight at once.  Warp w
+    // owns runs w, w + WARPS, ...; their descriptors are loaded by one lane
+    // each, all at once, and handed round by shuffles.
     constexpr uint32_t WARPS = TT / 32;
     for (uint32_t r0 = warp; r0 < rg.nreg; r0 += 32 * WARPS) {
         const uint32_t reg = r0 + lane * WARPS;
@@ -615,15 +636,17 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         if (reg < rg.nreg) {
             const RunInfo ri = tr[reg];
             goff = ri.goff;
-            loc = ri.loc;
-            end = reg + 1 < rg.nreg ? tr[reg + 1].loc : tcount;
+            end = ri.end;
+            loc = reg ? tr[reg - 1].end : 0u;
         }
         const uint32_t nrun = min(32u, (rg.nreg - r0 + WARPS - 1) / WARPS);
         for (uint32_t j = 0; j < nrun; ++j) {
             const uint32_t g = __shfl_sync(0xffffffffu, goff, j);
             const uint32_t l = __shfl_sync(0xffffffffu, loc, j);
             const uint32_t len = __shfl_sync(0xffffffffu, end, j) - l;
-            for (uint32_t t = lane; t < len; t += 32) cp_async4(&stage[l + t], res + g + t);
+            WRS_CHECK(g % RUN_ALIGN == 0 && l % RUN_ALIGN == 0 && len % RUN_ALIGN == 0 &&
+                      l + len <= stage_slots(rg.nreg, TT * RS_ROWS));
+            for (uint32_t t = 4 * lane; t < len; t += 128) cp_async16(&stage[l + t], res + g + t);
         }
     }
     cp_async_commit();
@@ -642,7 +665,7 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         }
     } else {
         for (uint32_t e = threadIdx.x; e < tcount; e += TT) {
-            WRS_CHECK(slot_of[tbase + e] < tcount);
+            WRS_CHECK(slot_of[tbase + e] < stage_slots(rg.nreg, TT * RS_ROWS));
             out[tbase + e] = stage[slot_of[tbase + e]] + out_base;
         }
     }
@@ -681,14 +704,15 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
-        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(0, 0);
+        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(REC_PAD, 0);
     }
     __shared__ uint4 bk_s[RC_ROWS * 256];
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
-                     ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
+        if (r[u].x != REC_PAD)  // (padding records: no draw)
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
+                         ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -696,7 +720,7 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
-        if (p < valid_end) {
+        if (p < valid_end && r[u].x != REC_PAD) {
             double x;
             if (W1) {
                 if constexpr (PHX)
@@ -994,15 +1018,18 @@ static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     p.rg.g = g;
     p.rg.shift = region_shift(g.n);
     p.rg.nreg = static_cast<uint32_t>((g.n + (1ull << p.rg.shift) - 1) >> p.rg.shift);
-    // expected draws per full region + ~20 sigma + a tile of slack
+    // expected draws per full region + ~20 sigma + two tiles of slack
     const double mu = static_cast<double>(chunk) *
                       (static_cast<double>(1ull << p.rg.shift) / static_cast<double>(g.n));
     p.tt = tile_threads_for(p.rg.nreg);
     p.tile = static_cast<uint32_t>(p.tt * RS_ROWS);
-    const double cap = mu + 20.0 * std::sqrt(mu) + 2.0 * p.tile;
+    // + the runs' padding: up to RUN_ALIGN - 1 slots per (tile, region)
+    const double pad = static_cast<double>(RUN_ALIGN - 1) * static_cast<double>((chunk + p.tile - 1) / p.tile);
+    const double cap = mu + 20.0 * std::sqrt(mu) + 2.0 * p.tile + pad;
     // slabs are whole multiples of the gather CTA's RC_SPAN positions
     auto round2k = [](uint64_t x) { return static_cast<uint32_t>((x + RC_SPAN - 1) / RC_SPAN * RC_SPAN); };
-    p.rg.cap = round2k(static_cast<uint64_t>(cap < static_cast<double>(chunk) ? cap : chunk) + p.tile);
+    const double most = static_cast<double>(chunk) + pad;  // every draw of the chunk in one region
+    p.rg.cap = round2k(static_cast<uint64_t>(cap < most ? cap : most) + p.tile);
     p.rg.ov_cap = round2k(chunk / 64 + 8 * p.tile);
     // tests: shrink the slabs to force the redirect / overflow paths
     if (const char* e = getenv("WRS_B200_TEST_SLAB_CAP")) p.rg.cap = round2k(strtoull(e, nullptr, 10));
@@ -1105,7 +1132,7 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
                                uint32_t* o, cudaStream_t st, bool on_side, cudaStream_t side,
                                cudaEvent_t side_ev) {
     const int sm_scatter = static_cast<int>(scatter_smem_bytes(rg.nreg, plan.tile));
-    const int sm_unperm = static_cast<int>(plan.tile * sizeof(uint32_t));
+    const int sm_unperm = static_cast<int>(stage_slots(rg.nreg, plan.tile) * sizeof(uint32_t));
     const bool w1 = g.W == 1;
     cudaStream_t ss = on_side ? side : st;
     poison(B.rec, plan.rec_slots * sizeof(uint2), ss);  // checked builds only
