@@ -2014,10 +2014,16 @@ k_pack(uint64_t P, DevScalars* sc, const double* __restrict__ lw, const double* 
 #ifndef K4B_SMEM_KB
 #define K4B_SMEM_KB 36
 #endif
-constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // 6 CTAs per SM
-constexpr uint32_t K4B_PAD = 64;  // heavy ids staged either side of the tile's own
+constexpr uint32_t K4B_SMEM = K4B_SMEM_KB * 1024;  // 5 CTAs per SM (the register budget)
+#ifndef K4B_KEEP
+#define K4B_KEEP 1  // the lights' weights from classify's registers (0.58 vs 0.60 ms)
+#endif
+#ifndef K4B_PAD_DEF
+#define K4B_PAD_DEF 64
+#endif
+constexpr uint32_t K4B_PAD = K4B_PAD_DEF;  // heavy ids staged either side of the tile's own
 #ifndef K4B_MINB
-#define K4B_MINB 6
+#define K4B_MINB 5
 #endif
 __global__ void __launch_bounds__(K1_THREADS, K4B_MINB)
 k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
@@ -2040,7 +2046,12 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     const uint64_t tile = blockIdx.x;
     const uint64_t base = tile * K1_TILE;
     const uint64_t nh = sc->nh;
+#if K4B_KEEP
+    double xs[K1_ROWS];  // the tile's weights stay in registers (no re-read for the lights)
+    classify_tile<true>(w, n, base, sc->wn, xs, C);
+#else
     classify_tile<false>(w, n, base, sc->wn, nullptr, C);
+#endif
     const unsigned lt = lanemask_lt();
     if (nh == 0) {  // fill_uniform_if_no_heavy (alias.hpp:288-297)
 #pragma unroll 4
@@ -2084,7 +2095,11 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
     __syncthreads();
     const uint32_t hmax = static_cast<uint32_t>(nh - 1);
     const uint32_t wlo32 = static_cast<uint32_t>(wlo), wn32 = static_cast<uint32_t>(whi - wlo);
+#if K4B_KEEP
+#pragma unroll
+#else
 #pragma unroll 4
+#endif
     for (int r = 0; r < K1_ROWS; ++r) {
         const uint64_t gi = base + r * K1_THREADS + threadIdx.x;
         if (gi >= n) continue;
@@ -2093,7 +2108,11 @@ k_assemble(const double* __restrict__ w, uint64_t n, const DevScalars* sc,
         double share;
         uint32_t rank;
         if ((lm >> lane) & 1) {
+#if K4B_KEEP
+            share = xs[r];
+#else
             share = __ldg(w + gi);
+#endif
             rank = min(d_la[C.exL[cell] + __popc(lm & lt)], hmax);  // heavy_at(j)
         } else {
             const uint32_t q = C.exH[cell] + __popc(C.hm[cell] & lt);
