@@ -1721,8 +1721,7 @@ __device__ __forceinline__ Boundary psa_boundary(uint64_t b, uint64_t n, uint64_
     return Boundary{static_cast<uint32_t>(np - lo), static_cast<uint32_t>(lo), spill};
 }
 
-// K3 as its own kernel (the pack computes the boundaries itself by default;
-// WRS_B200_K3=separate): one thread per boundary.
+// K3: one thread per boundary.
 __global__ void __launch_bounds__(256)
 k_split(uint64_t n, uint64_t P, const DevScalars* sc, SplitSrc S, uint32_t* split_l,
         uint32_t* split_h, double* split_s) {
