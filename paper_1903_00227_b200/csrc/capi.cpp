@@ -381,8 +381,15 @@ void sample_on(const wrs_sampler& s, uint64_t seed, uint64_t q0, uint64_t q1, ui
     ck(cudaStreamWaitEvent(s.side->s, s.sws_ev, 0), "wait");
     const int tb = s.front.load();
     if (s.dbuf) ck(cudaStreamWaitEvent(st, s.built_ev[tb], 0), "wait");
+    // The first scatter of a draw does not read the table, so it may run on
+    // the side stream under a preceding rebuild (WRS_B200_SIDE_SCATTER=1).
+    // Off by default: with both bandwidth-bound, the bench step measured
+    // 10.71 ms with the overlap vs 10.68 ms without.
+    const char* side_env = std::getenv("WRS_B200_SIDE_SCATTER");
+    const bool side_off = !(side_env && side_env[0] == '1');
     ck(wrsb::launch_sample(s.table(tb), s.n, s.wn, seed, stream_id, q0, q1, k, workers,
-                           base, out, st, &s.sws, s.side->s, s.side_ev),
+                           base, out, st, &s.sws, side_off ? nullptr : s.side->s,
+                           side_off ? nullptr : s.side_ev),
        "K5 launch");
     ck(cudaEventRecord(s.sws_ev, st), "event");
     if (s.dbuf) ck(cudaEventRecord(s.read_ev[tb], st), "event");

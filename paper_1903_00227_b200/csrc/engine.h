@@ -111,7 +111,8 @@ struct SampleWorkspace {
 // `stream_id` is the reference's sample stream 0x616c6961 ("alia").  `base` is
 // added to every output (global ids of a shard).  With a workspace, large
 // tables use the region-ordered plan; without, the direct gather kernel.
-// `side` (optional): a stream on which the region plan's first scatter runs.
+// `side` (optional; the C ABI passes it with WRS_B200_SIDE_SCATTER=1): a
+// stream on which the region plan's first scatter runs.
 // The scatter reads nothing but (n, seed, k), so it need not wait for the
 // table: it only waits for what `side` already carries (the previous user of
 // the scratch), and st waits for it (side_ev) before the first gather.  A

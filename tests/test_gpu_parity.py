@@ -383,11 +383,15 @@ def test_region_plan_draws_bit_exact(P, chunk, shift, monkeypatch):
     assert np.array_equal(S.draw(5, 6_000_011, 2), P.sample_many(b, S.bucket_mean, 5, 6_000_011, 2))
 
 
-def test_double_buffered_rebuild_then_draw_on_other_stream(P):
+@pytest.mark.parametrize("side", ["0", "1"])
+def test_double_buffered_rebuild_then_draw_on_other_stream(P, side, monkeypatch):
     """wrs_b200_sampler_double_buffer: the first rebuild writes the second
     (uninitialised) table on its own stream while a draw issued right after it
-    on another stream must wait for it; then pipelined rebuild/draw rounds."""
+    on another stream must wait for it; then pipelined rebuild/draw rounds.
+    side = "1": each draw's first scatter runs on the side stream, under the
+    rebuild (WRS_B200_SIDE_SCATTER)."""
     import torch
+    monkeypatch.setenv("WRS_B200_SIDE_SCATTER", side)
     n, k = 3_000_017, 4_000_003
     w = P.generate_uniform(n, 17)
     W, S = build(w)
