@@ -72,6 +72,8 @@ struct Workspace {
     double* hshare_own = nullptr;    // separate storage (else hshare aliases hpre)
     double* totals = nullptr;        // K2a block totals (light blocks, then heavy)
     double* carries = nullptr;       // K2b exclusive carries
+    double* bmax = nullptr;          // K2a (bulk form) per-block max weight, for K3's coarse brackets
+    bool coarse = false;             // bmax is valid for this build
     uint32_t* split_l = nullptr;     // K3 boundaries, P + 1
     uint32_t* split_h = nullptr;
     double* split_s = nullptr;       // spill entering each job

@@ -1341,7 +1341,7 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
                                         const DevScalars* sc, double* __restrict__ totals,
                                         double2* __restrict__ lck, double2* __restrict__ hck,
                                         const double* carries, const unsigned* flags,
-                                        uint64_t nb_flags) {
+                                        uint64_t nb_flags, double* __restrict__ bmax = nullptr) {
     const int lane = threadIdx.x & 31;
     const uint64_t nl = sc->nl, nh = sc->nh;
     const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
@@ -1397,6 +1397,11 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
     for (int c = 0; c < KB_NB; ++c)
         if (c < nch) issue(c);
     CompSumPos cs{0.0, 0.0};
+    // (K2a, heavy blocks) an upper bound of the block's weights for K3's
+    // coarse brackets: the largest high word (positive doubles order like
+    // their bit patterns), one integer max per element
+    const bool want_max = !CK && heavy && bmax;
+    int mxh = 0;
     if (CK && len > 0) {
         double carry;
         if (flags) {  // the chain CTA of this launch publishes the carries
@@ -1428,6 +1433,7 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
                     const double2 v = row[q * 16 + e];
                     cs.add(v.x);
                     cs.add(v.y);
+                    if (want_max) mxh = max(mxh, max(__double2hiint(v.x), __double2hiint(v.y)));
                 }
                 k1 = make_double2(cs.hi, cs.lo);
 #pragma unroll
@@ -1435,6 +1441,7 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
                     const double2 v = row[q * 16 + e];
                     cs.add(v.x);
                     cs.add(v.y);
+                    if (want_max) mxh = max(mxh, max(__double2hiint(v.x), __double2hiint(v.y)));
                 }
                 if (CK) {
                     double2* d = ck + (c * KB_C + q * 32) / CK_STRIDE;
@@ -1450,6 +1457,7 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
                 for (int e = 0; e < n32; ++e) {
                     if (e == CK_STRIDE) k1 = make_double2(cs.hi, cs.lo);
                     cs.add(row[q * 32 + e]);
+                    if (want_max) mxh = max(mxh, __double2hiint(row[q * 32 + e]));
                 }
                 if (CK) {
                     double2* d = ck + (c * KB_C + q * 32) / CK_STRIDE;
@@ -1461,20 +1469,23 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
         __syncwarp();
         if (c + KB_NB < nch) issue(c + KB_NB);
     }
-    if (!CK && len > 0) totals[b] = cs.value();  // carry[b] = local.value(), parallel.hpp:114
+    if (!CK && len > 0) {
+        totals[b] = cs.value();  // carry[b] = local.value(), parallel.hpp:114
+        if (want_max) bmax[b] = __hiloint2double(mxh, -1);  // >= every weight of the block
+    }
 }
 
 // K2a, bulk form: warp units in a grid stride.
 __global__ void __launch_bounds__(KB_WARPS * 32, 1)
 k_totals_kb(const double* __restrict__ lw, const double* __restrict__ hw, const DevScalars* sc,
-            double* __restrict__ totals, uint32_t wunits) {
+            double* __restrict__ totals, uint32_t wunits, double* __restrict__ bmax) {
     extern __shared__ __align__(128) unsigned char kbs[];
     KBWarp& W = reinterpret_cast<KBWarp*>(kbs)[threadIdx.x >> 5];
     kb_init(W);
     unsigned par = 0;
     for (uint32_t wu = blockIdx.x * KB_WARPS + (threadIdx.x >> 5); wu < wunits;
          wu += gridDim.x * KB_WARPS)
-        kb_unit<false>(wu, W, par, lw, hw, sc, totals, nullptr, nullptr, nullptr, nullptr, 0);
+        kb_unit<false>(wu, W, par, lw, hw, sc, totals, nullptr, nullptr, nullptr, nullptr, 0, bmax);
 }
 
 // K2c, bulk form, after a separate K2b (WRS_B200_K2_FUSE=0).
@@ -1659,7 +1670,27 @@ struct SplitSrc {
     CkList L, H;
     const double* hw;
     bool ckpt;
+    // coarse brackets (checkpoint form with the bulk-copy K2a): the carries
+    // (prefix at every block start; light blocks, then heavy from nbl) and
+    // the heavy blocks' largest weights decide most probes from L2-resident
+    // data before any checkpoint or weight is read
+    const double* carries;
+    const double* bmax;
+    bool coarse;
 };
+
+// prefix of a list at x from its block carries: between the carry of x's
+// block and the next (widened like ck_bracket; +inf past the last block)
+__device__ __forceinline__ void coarse_bracket(const double* car, uint64_t nb, uint64_t x,
+                                               double& lo, double& hi) {
+    if (x == 0) {
+        lo = hi = 0.0;
+        return;
+    }
+    const uint64_t blk = (x - 1) / SCAN_BLOCK;
+    lo = __ldg(car + blk) * (1.0 - 1e-13);
+    hi = blk + 1 < nb ? __ldg(car + blk + 1) * (1.0 + 1e-13) : CUDART_INF;
+}
 
 struct Boundary {
     uint32_t i, j;
@@ -1692,8 +1723,25 @@ __device__ __forceinline__ Boundary psa_boundary(uint64_t b, uint64_t n, uint64_
         if (mid >= nh) {
             above = true;  // f = inf
         } else {
-            const double w = __ldg(S.hw + mid);
-            if (!S.ckpt) {
+            int coarse = 2;  // 1: above, 0: not, 2: undecided
+            if (S.coarse) {
+                // f(mid) = (L(np - mid) + H(mid)) + w with w in (wn, block max]
+                // (heavies are > wn); floating-point + is monotone, so the
+                // bracket ends bound f
+                const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
+                const uint64_t nbh = (nh + SCAN_BLOCK - 1) / SCAN_BLOCK;
+                double l0, l1, h0, h1;
+                coarse_bracket(S.carries, nbl, np - mid, l0, l1);
+                coarse_bracket(S.carries + nbl, nbh, mid, h0, h1);
+                if ((l0 + h0) + wn > target)
+                    coarse = 1;
+                else if ((l1 + h1) + __ldg(S.bmax + nbl + mid / SCAN_BLOCK) <= target)
+                    coarse = 0;
+            }
+            const double w = coarse == 2 ? __ldg(S.hw + mid) : 0.0;
+            if (coarse != 2) {
+                above = coarse == 1;
+            } else if (!S.ckpt) {
                 above = (__ldg(S.lpre + (np - mid)) + __ldg(S.hpre + mid)) + w > target;
             } else {
                 double l0, l1, h0, h1;
@@ -2168,6 +2216,7 @@ cudaError_t workspace_alloc(Workspace& ws, uint64_t n, uint64_t P, bool separate
     A(ws.hpre, n + 1);
     A(ws.totals, nblocks);
     A(ws.carries, nblocks);
+    A(ws.bmax, nblocks);
     A(ws.lck, n / CK_STRIDE + 2);
     A(ws.hck, n / CK_STRIDE + 2);
     A(ws.split_l, P + 1);
@@ -2204,7 +2253,8 @@ void workspace_free(Workspace& ws) {
     void* ptrs[] = {ws.node_val, ws.node_cnt, ws.tile_status, ws.hidx,       ws.lw,
                     ws.hw,       ws.lpre,     ws.hpre,        ws.totals,
                     ws.carries,  ws.split_l,  ws.split_h,     ws.split_s,    ws.sc,
-                    ws.lrank_own, ws.hshare_own, ws.lck,       ws.hck,    ws.k2_flags};
+                    ws.lrank_own, ws.hshare_own, ws.lck,       ws.hck,    ws.k2_flags,
+                    ws.bmax};
     for (void* p : ptrs)
         if (p) dev_free(p);
     ws = Workspace{};
@@ -2282,6 +2332,12 @@ static int sm_count_psa() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return sms;
+}
+
+// K3's coarse brackets from block carries + block maxima (WRS_B200_K3_COARSE=0: off).
+static bool k3_coarse_enabled() {
+    const char* e = std::getenv("WRS_B200_K3_COARSE");
+    return !(e && e[0] == '0');
 }
 
 // Bulk-copy K2a / K2c (WRS_B200_K2_KB=0: the smem-staged kernels).
@@ -2390,7 +2446,8 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
         k_scan_totals_bulk<CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.sc,
                                                                           ws.totals);
     else if (kb)
-        k_totals_kb<<<kb_grid, KB_WARPS * 32, KB_SMEM, st>>>(ws.lw, ws.hw, ws.sc, ws.totals, kb_units);
+        k_totals_kb<<<kb_grid, KB_WARPS * 32, KB_SMEM, st>>>(ws.lw, ws.hw, ws.sc, ws.totals, kb_units,
+                                                             ws.bmax);
     else
         K2_LAUNCH(false);
     REC(2);
@@ -2426,7 +2483,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     REC(4);
     {
         SplitSrc src{ws.lpre, ws.hpre, CkList{ws.lw, ws.lck, 0}, CkList{ws.hw, ws.hck, 0}, ws.hw,
-                     ws.ckpt};
+                     ws.ckpt, ws.carries, ws.bmax, ws.ckpt && kb && k3_coarse_enabled()};
         const unsigned grid = static_cast<unsigned>((P + 1 + 255) / 256);
         k_split<<<grid, 256, 0, st>>>(n, P, ws.sc, src, ws.split_l, ws.split_h, ws.split_s);
     }
