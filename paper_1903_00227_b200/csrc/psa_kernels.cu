@@ -622,10 +622,15 @@ constexpr int K2F_S = K2F_S_DEF;  // totals per chain chunk (publication granula
 __host__ __device__ inline uint64_t k2_flag_slots(uint64_t n) {
     return ((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 2 + K2F_S - 1) / K2F_S + 1;
 }
-__host__ __device__ inline uint64_t k2_flag_words(uint64_t n) { return 2 * 32 * k2_flag_slots(n); }
+// (flag lines, then the same number of count lines: K2a units completed per
+// chunk of K2F_S blocks, for the launch that also runs K2a)
+__host__ __device__ inline uint64_t k2_flag_words(uint64_t n) { return 4 * 32 * k2_flag_slots(n); }
 __device__ __forceinline__ const unsigned* k2_flag(const unsigned* f, bool heavy, uint64_t slots,
                                                    uint64_t chunk) {
     return f + 32 * ((heavy ? slots : 0) + chunk);
+}
+__device__ __forceinline__ unsigned* k2_tdone(unsigned* f, bool heavy, uint64_t slots, uint64_t chunk) {
+    return f + 32 * (2 * slots + (heavy ? slots : 0) + chunk);
 }
 
 // One warp's 32 block chains of K2c (warp unit `wu` of the launch).  done
@@ -1128,7 +1133,7 @@ template <int K2W_S, int D = 1, int RX = 3>
 __device__ __forceinline__ void carry_chain(bool heavy, double* k2w, const DevScalars* sc,
                                             const double* __restrict__ totals, double* carries,
                                             double* lpre, double* hpre, unsigned* done,
-                                            uint64_t nb_flags) {
+                                            uint64_t nb_flags, bool wait_totals = false) {
     static_assert(RX >= D + 2, "x ring too short for the prefetch depth");
     double* X = k2w;             // [RX][S] totals
     double* T = X + RX * K2W_S;  // [4][S] hi after each add
@@ -1152,6 +1157,15 @@ __device__ __forceinline__ void carry_chain(bool heavy, double* k2w, const DevSc
     auto load = [&](int c) {
         if (c < nch) {
             const int cnt = cnt_of(c);
+            if (wait_totals) {  // the chunk's K2a units (same launch) have stored its totals
+                if (lane == 0) {
+                    const unsigned* t = k2_tdone(done, heavy, nb_flags, c);
+                    while (*reinterpret_cast<const volatile unsigned*>(t) < static_cast<unsigned>(cnt))
+                        __nanosleep(128);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                __syncwarp();
+            }
             double* xb = X + (c % RX) * K2W_S;
             for (int i = lane; i < cnt; i += 32)
                 cp_async8(xb + i, src + static_cast<uint64_t>(c) * K2W_S + i);
@@ -1341,7 +1355,8 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
                                         const DevScalars* sc, double* __restrict__ totals,
                                         double2* __restrict__ lck, double2* __restrict__ hck,
                                         const double* carries, const unsigned* flags,
-                                        uint64_t nb_flags, double* __restrict__ bmax = nullptr) {
+                                        uint64_t nb_flags, double* __restrict__ bmax = nullptr,
+                                        unsigned* tdone = nullptr) {
     const int lane = threadIdx.x & 31;
     const uint64_t nl = sc->nl, nh = sc->nh;
     const uint64_t nbl = (nl + SCAN_BLOCK - 1) / SCAN_BLOCK;
@@ -1473,6 +1488,12 @@ __device__ __forceinline__ void kb_unit(uint64_t wu, KBWarp& W, unsigned& par,
         totals[b] = cs.value();  // carry[b] = local.value(), parallel.hpp:114
         if (want_max) bmax[b] = __hiloint2double(mxh, -1);  // >= every weight of the block
     }
+    if (!CK && tdone) {  // one launch with the chain: count this unit's totals in
+        __threadfence();
+        const unsigned done = __popc(__ballot_sync(0xffffffffu, len > 0));
+        if (lane == 0 && done)
+            atomicAdd(k2_tdone(tdone, heavy, nb_flags, (idx * 32) / K2F_S), done);
+    }
 }
 
 // K2a, bulk form: warp units in a grid stride.
@@ -1517,10 +1538,10 @@ constexpr int K2F_D = 4, K2F_RX = 6;  // chain prefetch depth / x ring (loaded L
 constexpr int K2F_SMEM = KB_SMEM > k2w_smem(K2F_S, K2F_RX) ? KB_SMEM : k2w_smem(K2F_S, K2F_RX);
 constexpr int K2F_THREADS = 32 * (KB_WARPS > 5 ? KB_WARPS : 5);  // chain: 5 warps
 __global__ void __launch_bounds__(K2F_THREADS, 1)
-k_carry_ckpt(DevScalars* sc, const double* __restrict__ totals, double* carries, double* lpre,
+k_carry_ckpt(DevScalars* sc, double* totals, double* carries, double* lpre,
              double* hpre, const double* __restrict__ lw, const double* __restrict__ hw,
              double2* __restrict__ lck, double2* __restrict__ hck, unsigned* flags,
-             uint64_t nb_flags, uint32_t wunits) {
+             uint64_t nb_flags, uint32_t wunits, uint32_t units_a, double* bmax) {
     extern __shared__ __align__(128) double k2f[];
     __shared__ unsigned role;
     if (threadIdx.x == 0) role = atomicAdd(&sc->k2_ticket, 1u);
@@ -1528,7 +1549,7 @@ k_carry_ckpt(DevScalars* sc, const double* __restrict__ totals, double* carries,
     const unsigned t = role;
     if (t < 2) {
         carry_chain<K2F_S, K2F_D, K2F_RX>(t == 1, k2f, sc, totals, carries, lpre, hpre, flags,
-                                          nb_flags);
+                                          nb_flags, units_a > 0);
         return;
     }
     const int wq = threadIdx.x >> 5;
@@ -1537,12 +1558,20 @@ k_carry_ckpt(DevScalars* sc, const double* __restrict__ totals, double* carries,
     kb_init(W);
     unsigned par = 0;
     const int lane = threadIdx.x & 31;
-    for (;;) {  // units in order: the earliest carries are published first
+    // units in order: with units_a > 0 (K2a in this launch too) the K2a units
+    // come first -- none of them waits on anything, so the chains they feed
+    // always progress -- then the checkpoint units, earliest carries first
+    for (;;) {
         unsigned wu = 0;
         if (lane == 0) wu = atomicAdd(&sc->k2_work, 1u);
         wu = __shfl_sync(0xffffffffu, wu, 0);
-        if (wu >= wunits) break;
-        kb_unit<true>(wu, W, par, lw, hw, sc, nullptr, lck, hck, carries, flags, nb_flags);
+        if (wu >= units_a + wunits) break;
+        if (wu < units_a)
+            kb_unit<false>(wu, W, par, lw, hw, sc, totals, nullptr, nullptr, nullptr, nullptr,
+                           nb_flags, bmax, flags);
+        else
+            kb_unit<true>(wu - units_a, W, par, lw, hw, sc, nullptr, lck, hck, carries, flags,
+                          nb_flags);
     }
 }
 
@@ -2346,10 +2375,15 @@ static bool k2_kb_enabled() {
     return !(e && e[0] == '0');
 }
 
-// K2b fused with the checkpoint pass (WRS_B200_K2_FUSE=0: two kernels).
+// K2a, K2b and the checkpoint pass in one launch (default);
+// WRS_B200_K2_FUSE=1: K2a separate; =0: three kernels.
 static bool k2_fuse_enabled() {
     const char* e = std::getenv("WRS_B200_K2_FUSE");
     return !(e && e[0] == '0');
+}
+static bool k2_fuse_all_enabled() {
+    const char* e = std::getenv("WRS_B200_K2_FUSE");
+    return !(e && (e[0] == '0' || e[0] == '1'));
 }
 
 cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64_t P,
@@ -2437,18 +2471,24 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     // large tables: the bulk-copy forms of K2a / K2c (WRS_B200_K2_KB=0: the
     // smem-staged forms)
     const bool kb = pos && !split && !direct && k2_kb_enabled();
+    // ... and K2a in the same launch as the chain and the checkpoints (see
+    // k_carry_ckpt; WRS_B200_K2_FUSE=1 launches K2a on its own)
+    const bool bulk_exp = pos && !split && !direct && std::getenv("WRS_B200_K2_BULK");
+    const bool fuse_all = kb && k2_ckpt_enabled() && k2_fuse_all_enabled() && !bulk_exp;
+    // K2a's bulk form also bounds every heavy block's weights (K3's coarse brackets)
+    const bool have_bmax = kb && !bulk_exp;
     const int sms = sm_count_psa();
     // per-list units: nlu + nhu <= (blocks + 31) / 32 + 1 (empty ones return at once)
     const uint32_t kb_units = static_cast<uint32_t>((nblocks + 31) / 32 + 1);
     const unsigned kb_grid = static_cast<unsigned>(
         std::min<uint64_t>((kb_units + KB_WARPS - 1) / KB_WARPS, sms));
-    if (pos && !split && !direct && std::getenv("WRS_B200_K2_BULK"))
+    if (bulk_exp)
         k_scan_totals_bulk<CompSumPos><<<k2_grid, K2_WARPS * 32, 0, st>>>(ws.lw, ws.hw, ws.sc,
                                                                           ws.totals);
-    else if (kb)
+    else if (kb && !fuse_all)
         k_totals_kb<<<kb_grid, KB_WARPS * 32, KB_SMEM, st>>>(ws.lw, ws.hw, ws.sc, ws.totals, kb_units,
                                                              ws.bmax);
-    else
+    else if (!fuse_all)
         K2_LAUNCH(false);
     REC(2);
     // large tables: checkpoints instead of full prefix arrays (1 B per item
@@ -2464,7 +2504,8 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
         if (e != cudaSuccess) return e;
         k_carry_ckpt<<<grid, K2F_THREADS, K2F_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre,
                                                   ws.lw, ws.hw, ws.lck, ws.hck, ws.k2_flags,
-                                                  k2_flag_slots(ws.n), kb_units);
+                                                  k2_flag_slots(ws.n), kb_units,
+                                                  fuse_all ? kb_units : 0u, ws.bmax);
     } else if (pos) {
         k_scan_carry_split<<<2, 160, K2W_SMEM, st>>>(ws.sc, ws.totals, ws.carries, ws.lpre, ws.hpre);
     } else {
@@ -2483,7 +2524,7 @@ cudaError_t launch_psa_build(const double* d_w, uint64_t n, double total, uint64
     REC(4);
     {
         SplitSrc src{ws.lpre, ws.hpre, CkList{ws.lw, ws.lck, 0}, CkList{ws.hw, ws.hck, 0}, ws.hw,
-                     ws.ckpt, ws.carries, ws.bmax, ws.ckpt && kb && k3_coarse_enabled()};
+                     ws.ckpt, ws.carries, ws.bmax, ws.ckpt && have_bmax && k3_coarse_enabled()};
         const unsigned grid = static_cast<unsigned>((P + 1 + 255) / 256);
         k_split<<<grid, 256, 0, st>>>(n, P, ws.sc, src, ws.split_l, ws.split_h, ws.split_s);
     }

@@ -48,6 +48,7 @@ def main():
     # bulk-copy with a separate K2b, and the smem-staged kernels
     forms = {"split": (big, big, {}), "direct": ("0", big, {}), "staged": ("0", "0", {}),
              "staged-nofuse": ("0", "0", {"WRS_B200_K2_FUSE": "0"}),
+             "staged-fuse1": ("0", "0", {"WRS_B200_K2_FUSE": "1"}),
              "staged-nokb": ("0", "0", {"WRS_B200_K2_KB": "0"})}
     for form, (smax, dmax, extra) in forms.items():
         os.environ["WRS_B200_K2_SPLIT_MAX"] = smax

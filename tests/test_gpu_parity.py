@@ -123,7 +123,7 @@ def check_checkpoints(ck, prefix, x):
 
 @pytest.mark.parametrize("k2", ["split", "direct", "direct-lpw1", "direct-lpw32", "staged",
                                 "staged-k1staged", "staged-k2bulk", "staged-nofuse",
-                                "staged-nokb"])
+                                "staged-fuse1", "staged-nokb"])
 def test_stages_bit_exact(P, k2, monkeypatch):
     if k2.endswith("k1staged"):  # K1's staged form (the unstaged one is the default)
         monkeypatch.setenv("WRS_B200_K1", "staged")
@@ -131,8 +131,11 @@ def test_stages_bit_exact(P, k2, monkeypatch):
     if k2.endswith("k2bulk"):  # K2a through TMA bulk copies (measured slower, opt-in)
         monkeypatch.setenv("WRS_B200_K2_BULK", "1")
         k2 = k2.split("-")[0]
-    if k2.endswith("nofuse"):  # K2b and the checkpoint pass as two kernels
+    if k2.endswith("nofuse"):  # K2a, K2b and the checkpoint pass as three kernels
         monkeypatch.setenv("WRS_B200_K2_FUSE", "0")
+        k2 = k2.split("-")[0]
+    if k2.endswith("fuse1"):  # K2a on its own, K2b fused with the checkpoint pass
+        monkeypatch.setenv("WRS_B200_K2_FUSE", "1")
         k2 = k2.split("-")[0]
     if k2.endswith("nokb"):  # the smem-staged K2a / K2c instead of the bulk-copy forms
         monkeypatch.setenv("WRS_B200_K2_KB", "0")
