@@ -33,6 +33,7 @@
 //   the Philox mode is a compile-time variant of every draw kernel.
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "engine.h"
@@ -337,9 +338,9 @@ constexpr uint32_t REC_PAD = 0xffffffffu;  // (draw indices within a chunk are <
 __host__ __device__ inline uint32_t stage_slots(uint32_t nreg, uint32_t tile) {
     return tile + (RUN_ALIGN - 1) * nreg;
 }
-__host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t tile) {
+__host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t tile, size_t rec_bytes) {
     const size_t head = (4 * static_cast<size_t>(nreg) + 2) * 4;
-    return ((head + 15) & ~size_t(15)) + stage_slots(nreg, tile) * sizeof(uint2);
+    return ((head + 15) & ~size_t(15)) + stage_slots(nreg, tile) * rec_bytes;
 }
 
 // ORDER = false (aggregated draws): the answers are only counted, never put
@@ -369,15 +370,20 @@ constexpr int RC_SPAN = RC_ROWS * 256;  // slab positions per gather / count CTA
 template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS, bool FULL = false>
 __global__ void __launch_bounds__(TT, RS_MIN_CTAS * 256 / TT)
 k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
-                 unsigned* __restrict__ overflow, uint2* __restrict__ rec,
+                 unsigned* __restrict__ overflow, void* __restrict__ rec_out,
                  uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
+    // plain draws: 4-B records, the draw's index in the chunk (the gather
+    // recomputes its bucket and coin from the counter-based stream);
+    // aggregated draws: {draw index, bucket}
+    using Rec = std::conditional_t<ORDER, uint32_t, uint2>;
+    Rec* const rec = static_cast<Rec*>(rec_out);
     extern __shared__ __align__(16) unsigned char rs_smem[];
     const uint32_t nreg = rg.nreg;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(rs_smem);  // [nreg] draws per region
     uint32_t* start = cnt + nreg;                          // [nreg + 1] run starts in the stage
     uint32_t* fill = start + nreg + 1;                     // [nreg] fill cursors
     uint32_t* goff = fill + nreg;                          // [nreg] the runs' slab positions
-    uint2* stage = reinterpret_cast<uint2*>(rs_smem + (((4 * nreg + 2) * 4 + 15) & ~15u));  // padded runs
+    Rec* stage = reinterpret_cast<Rec*>(rs_smem + (((4 * nreg + 2) * 4 + 15) & ~15u));  // padded runs
     const uint64_t tile = static_cast<uint64_t>(tile0) + blockIdx.x;
     const uint64_t tbase = tile * (TT * RS_ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -466,7 +472,10 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
         if (ORDER) runs[tile * nreg + reg] = RunInfo{goff[reg], start[reg + 1]};
         for (uint32_t i = start[reg] + cnt[reg]; i < start[reg + 1]; ++i)
-            stage[i] = make_uint2(REC_PAD, 0u);
+            if constexpr (ORDER)
+                stage[i] = REC_PAD;
+            else
+                stage[i] = make_uint2(REC_PAD, 0u);
     }
     const uint32_t t32 = static_cast<uint32_t>(tbase);
 #pragma unroll
@@ -474,8 +483,12 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         const uint32_t e = r * TT + threadIdx.x;
         if (e < kc_left) {
             const uint32_t slot = atomicAdd(&fill[bk[r] >> rg.shift], 1u);
-            stage[slot] = make_uint2(t32 + e, bk[r]);
-            if (ORDER) slot_of[tbase + e] = static_cast<uint16_t>(slot);
+            if constexpr (ORDER) {
+                stage[slot] = t32 + e;
+                slot_of[tbase + e] = static_cast<uint16_t>(slot);
+            } else {
+                stage[slot] = make_uint2(t32 + e, bk[r]);
+            }
         }
     }
     // (no early exit on overflow: an overflowed run is written to the start
@@ -495,7 +508,8 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
                       goff[reg] + len <= static_cast<uint64_t>(rg.nreg) * rg.cap + rg.ov_cap);
             const unsigned src = static_cast<unsigned>(__cvta_generic_to_shared(stage + start[reg]));
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
-                         :: "l"(rec + goff[reg]), "r"(src), "r"(len * 8u), "l"(pol) : "memory");
+                         :: "l"(rec + goff[reg]), "r"(src),
+                            "r"(len * static_cast<uint32_t>(sizeof(Rec))), "l"(pol) : "memory");
             issued = true;
         }
     }
@@ -526,7 +540,7 @@ __device__ __forceinline__ uint64_t slab_valid_end(const RegionGeom& rg, const u
 template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(256, RC_MIN_CTAS)
 k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
-                const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
+                const unsigned* __restrict__ overflow, const uint32_t* __restrict__ rec,
                 uint32_t* __restrict__ res) {
     if (*overflow) return;  // the overflow slab overflowed: RD recomputes the chunk directly
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
@@ -535,15 +549,25 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
     const uint64_t key0 = rng_derive(rg.g.base_key, 0);  // W1: the single worker's key
-    uint2 r[RC_ROWS];
+    const uint32_t n32 = static_cast<uint32_t>(rg.g.n);
+    // the records are draw indices: each draw's counter, bucket and coin are
+    // recomputed here from the counter-based stream (the gather has issue
+    // slots to spare; the scatter writes and this kernel reads 4 B per
+    // record instead of 8)
+    auto ctr1 = [&](uint32_t e) -> uint64_t {
+        const uint64_t q = rg.q0 + e;
+        if (W1) return key0 + (2 * q + 1) * kGolden;
+        uint32_t w;
+        uint64_t m;
+        locate(rg.g, q, w, m);
+        return kc.get(rg.g, w) + (2 * m + 1) * kGolden;
+    };
+    uint32_t r[RC_ROWS];
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
-        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(REC_PAD, 0);
+        r[u] = p < valid_end ? ld_stream(rec + p, pf) : REC_PAD;
     }
-#pragma unroll
-    for (int u = 0; u < RC_ROWS; ++u)
-        WRS_CHECK(p0 + u * 256 + threadIdx.x >= valid_end || r[u].y < rg.g.n);
     // bucket gathers as LDGSTS into shared memory: measured 232 G random
     // L2-resident 16-B rows/s vs 200 G for LDG (scripts/microbench/
     // l2_gather_bench.cu); each thread reads back only its own rows.
@@ -552,9 +576,16 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
-        if (r[u].x != REC_PAD)
+        if (r[u] != REC_PAD) {
+            uint32_t bi;
+            if constexpr (PHX)
+                bi = philox_bucket(rg.g, rg.q0 + r[u]);
+            else
+                bi = mulhi_n32(mix64(ctr1(r[u])), n32);
+            WRS_CHECK(bi < rg.g.n);
             asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
-                         ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
+                         ::"r"(s), "l"(b + bi), "l"(pl) : "memory");
+        }
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -562,19 +593,12 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
-        if (p < valid_end && r[u].x != REC_PAD) {
+        if (r[u] != REC_PAD) {  // (positions past valid_end read as padding)
             double x;
-            if (W1) {
-                if constexpr (PHX)
-                    x = philox_coin(rg.g, rg.q0 + r[u].x);
-                else
-                    x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
-            } else {
-                uint32_t w;
-                uint64_t m;
-                locate(rg.g, rg.q0 + r[u].x, w, m);
-                x = draw_coin(rg.g, kc.get(rg.g, w), m);
-            }
+            if constexpr (PHX)
+                x = philox_coin(rg.g, rg.q0 + r[u]);
+            else
+                x = coin_of_ctr(rg.g, ctr1(r[u]));
             st_stream(res + p, pick(bk, x), pf);
         }
     }
@@ -1131,11 +1155,11 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
                                const Bucket* d_b, const RegionBuffers& B, uint32_t base,
                                uint32_t* o, cudaStream_t st, bool on_side, cudaStream_t side,
                                cudaEvent_t side_ev) {
-    const int sm_scatter = static_cast<int>(scatter_smem_bytes(rg.nreg, plan.tile));
+    const int sm_scatter = static_cast<int>(scatter_smem_bytes(rg.nreg, plan.tile, sizeof(uint32_t)));
     const int sm_unperm = static_cast<int>(stage_slots(rg.nreg, plan.tile) * sizeof(uint32_t));
     const bool w1 = g.W == 1;
     cudaStream_t ss = on_side ? side : st;
-    poison(B.rec, plan.rec_slots * sizeof(uint2), ss);  // checked builds only
+    poison(B.rec, plan.rec_slots * sizeof(uint32_t), ss);  // checked builds only (4-B records)
     poison(B.res, plan.rec_slots * sizeof(uint32_t), ss);
     cudaError_t e = reset_cursors(rg, B, ss);
     if (e != cudaSuccess) return e;
@@ -1155,21 +1179,21 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
         cudaFuncSetAttribute(k_region_unpermute<true, true, TT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
         k_region_gather<true, true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.overflow, B.rec, B.res);
+            rg, d_b, B.cursor, B.overflow, reinterpret_cast<const uint32_t*>(B.rec), B.res);
         k_region_unpermute<true, true, TT><<<tiles, TT, sm_unperm, st>>>(
             rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
     } else if (w1) {
         cudaFuncSetAttribute(k_region_unpermute<true, false, TT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
         k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.overflow, B.rec, B.res);
+            rg, d_b, B.cursor, B.overflow, reinterpret_cast<const uint32_t*>(B.rec), B.res);
         k_region_unpermute<true, false, TT><<<tiles, TT, sm_unperm, st>>>(
             rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
     } else {
         cudaFuncSetAttribute(k_region_unpermute<false, false, TT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
         k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.overflow, B.rec, B.res);
+            rg, d_b, B.cursor, B.overflow, reinterpret_cast<const uint32_t*>(B.rec), B.res);
         k_region_unpermute<false, false, TT><<<tiles, TT, sm_unperm, st>>>(
             rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
     }
@@ -1308,7 +1332,7 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
         if ((e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr))) != cudaSuccess) return e;
         region_bytes(plan, chunk, &B, ws->base);
         ws->overflow = B.overflow;
-        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg, plan.tile));
+        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg, plan.tile, sizeof(uint2)));
     }
     const unsigned fold_blocks = static_cast<unsigned>(
         umin64((n + 255) / 256, static_cast<uint64_t>(sm_count()) * 8));
