@@ -591,3 +591,22 @@ def test_psa_exact_env_gives_the_reference_table(P, monkeypatch):
     S = wrs.Sampler.build(W, "psa", 8)
     assert S.jobs == 8
     assert_same_table(S, w, 8, P)
+
+
+def test_host_output_draws_span_several_copy_chunks(P):
+    """wrs_sampler_draw into host memory copies out in 2^26-draw chunks while
+    the next chunk draws: more than one chunk, a ragged last one, both plans
+    (region plan on a 150-MB table) equal the device draw, itself pinned to
+    the oracle by the tests above."""
+    import torch
+    k = (1 << 26) * 2 + 12_345
+    for n in (1_000_003, 9_500_003):
+        w = P.generate_uniform(n, 23)
+        W, S = build(w)
+        host = S.draw(31, k, 3)
+        dev = torch.empty(k, dtype=torch.int32, device="cuda")
+        S.draw_device(31, k, 3, dev)
+        torch.cuda.synchronize()
+        assert np.array_equal(host, dev.cpu().numpy().view(np.uint32)), n
+        ref = P.sample_many(S.buckets(), S.bucket_mean, 31, 1_000_000, 3)
+        assert np.array_equal(S.draw(31, 1_000_000, 3), ref)
