@@ -1167,8 +1167,17 @@ __device__ __forceinline__ void carry_chain(bool heavy, double* k2w, const DevSc
                 __syncwarp();
             }
             double* xb = X + (c % RX) * K2W_S;
-            for (int i = lane; i < cnt; i += 32)
-                cp_async8(xb + i, src + static_cast<uint64_t>(c) * K2W_S + i);
+            if (wait_totals) {
+                // totals written during this launch: L2 loads (a cp.async may
+                // allocate the line in L1, and a line straddling the previous
+                // chunk -- the heavy list starts at block nbl -- could then be
+                // served stale)
+                for (int i = lane; i < cnt; i += 32)
+                    xb[i] = __ldcg(src + static_cast<uint64_t>(c) * K2W_S + i);
+            } else {
+                for (int i = lane; i < cnt; i += 32)
+                    cp_async8(xb + i, src + static_cast<uint64_t>(c) * K2W_S + i);
+            }
         }
         cp_async_commit();
     };
