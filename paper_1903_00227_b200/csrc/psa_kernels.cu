@@ -748,24 +748,6 @@ k_scan_blocks_ckpt(const double* __restrict__ lw, const double* __restrict__ hw,
 // global memory) with cp.async.bulk into 16-B-aligned shared rows, completion
 // counted on a per-warp, per-buffer mbarrier; the lanes then read their rows
 // as 16-B pairs (conflict-free at a 34-double row stride).
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(cnt));
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
-                 "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n"
-        ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
-                   "r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
-}
-
 template <class CS>
 __global__ void __launch_bounds__(K2_WARPS * 32)
 k_scan_totals_bulk(const double* __restrict__ lw, const double* __restrict__ hw, const DevScalars* sc,

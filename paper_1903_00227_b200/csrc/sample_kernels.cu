@@ -501,7 +501,10 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     __syncthreads();
     const uint64_t pol = policy_evict_first();
     bool issued = false;
-    for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
+    // run reg is issued by lane reg / WARPS of warp reg % WARPS: the per-lane
+    // issue loop the bulk copy compiles to is spread over every warp
+    constexpr uint32_t WARPS = TT / 32;
+    for (uint32_t reg = warp + WARPS * lane; reg < nreg; reg += TT) {
         const uint32_t len = start[reg + 1] - start[reg];
         if (len) {
             WRS_CHECK(goff[reg] % RUN_ALIGN == 0 &&
@@ -609,7 +612,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
 // then picks its answer at the slot RB recorded for it.  If a slab ever
 // overflowed (not expected: ~20 sigma of slack), the tile recomputes its
 // draws directly instead, so the output is correct in every case.
-template <bool W1, bool PHX = false, int TT = RS_THREADS>
+template <bool W1, bool PHX = false, int TT = RS_THREADS, bool BULK = true>
 __global__ void __launch_bounds__(TT, RD_MIN_CTAS * 256 / TT)
 k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
                    const unsigned* __restrict__ overflow, const RunInfo* __restrict__ runs,
@@ -648,13 +651,35 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         for (int i = 0; i < VP; ++i)
             sv[i] = *reinterpret_cast<const uint2*>(slot_of + tbase + (i * TT + threadIdx.x) * 4);
     }
+    constexpr uint32_t WARPS = TT / 32;
+    if constexpr (BULK) {
+        // this tile's runs -> shared memory, one cp.async.bulk per run (runs
+        // are padded to 4 results: 16-B aligned and sized on both sides),
+        // completion counted on one mbarrier expecting the tile's padded
+        // total.  Run reg is issued by lane reg / WARPS of warp reg % WARPS,
+        // so the per-lane issue loop the bulk copy compiles to stays short in
+        // every warp.  (~11 instructions per run instead of ~50 for a warp-
+        // wide LDGSTS loop: the difference at 256 regions per tile, n = 2^30.)
+        __shared__ uint64_t mbar;
+        if (threadIdx.x == 0) mbar_init(&mbar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_expect(&mbar, tr[rg.nreg - 1].end * 4u);
+        for (uint32_t reg = warp + WARPS * lane; reg < rg.nreg; reg += 32 * WARPS) {
+            const uint32_t loc = reg ? tr[reg - 1].end : 0u;
+            const RunInfo ri = tr[reg];
+            const uint32_t len = ri.end - loc;
+            WRS_CHECK(ri.goff % RUN_ALIGN == 0 && loc % RUN_ALIGN == 0 && len % RUN_ALIGN == 0 &&
+                      ri.end <= stage_slots(rg.nreg, TT * RS_ROWS));
+            if (len) bulk_g2s(&stage[loc], res + ri.goff, len * 4u, &mbar);
+        }
+        mbar_wait(&mbar, 0);
+    }
     // this tile's runs -> shared memory with 16-B LDGSTS (runs are padded to
     // 4 results, 16-B aligned in the slab and the stage): no register
     // staging, so every element of the tile is in flight at once.  Warp w
     // owns runs w, w + WARPS, ...; their descriptors are loaded by one lane
     // each, all at once, and handed round by shuffles.
-    constexpr uint32_t WARPS = TT / 32;
-    for (uint32_t r0 = warp; r0 < rg.nreg; r0 += 32 * WARPS) {
+    for (uint32_t r0 = warp; r0 < (BULK ? 0u : rg.nreg); r0 += 32 * WARPS) {
         const uint32_t reg = r0 + lane * WARPS;
         uint32_t goff = 0, loc = 0, end = 0;
         if (reg < rg.nreg) {
@@ -673,9 +698,11 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
             for (uint32_t t = 4 * lane; t < len; t += 128) cp_async16(&stage[l + t], res + g + t);
         }
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
+    if constexpr (!BULK) {
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+    }
     if (vec) {
 #pragma unroll
         for (int i = 0; i < VP; ++i) {
@@ -1148,6 +1175,21 @@ static void launch_scatter(const RegionGeom& rg, const RegionBuffers& B, int sme
     }
 }
 
+// RD staging: one bulk copy per run (default) or warp-wide 16-B LDGSTS
+// loops (WRS_B200_RD_BULK=0, the earlier form, kept for A/B and tests).
+static bool rd_bulk() {
+    const char* e = getenv("WRS_B200_RD_BULK");
+    return !(e && e[0] == '0');
+}
+template <bool W1, bool PHX, int TT, bool BULK>
+static void launch_unpermute(const RegionGeom& rg, const Bucket* d_b, const RegionBuffers& B,
+                             uint32_t base, uint32_t* o, unsigned tiles, int smem, cudaStream_t st) {
+    cudaFuncSetAttribute(k_region_unpermute<W1, PHX, TT, BULK>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_region_unpermute<W1, PHX, TT, BULK><<<tiles, TT, smem, st>>>(
+        rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
+}
+
 // One chunk of the region plan with TT-thread tiles: RB (on the side stream
 // when asked), then RC and RD on st.
 template <int TT>
@@ -1175,28 +1217,24 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
         if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
     }
-    if (g.philox) {
-        cudaFuncSetAttribute(k_region_unpermute<true, true, TT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
-        k_region_gather<true, true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.overflow, reinterpret_cast<const uint32_t*>(B.rec), B.res);
-        k_region_unpermute<true, true, TT><<<tiles, TT, sm_unperm, st>>>(
-            rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
-    } else if (w1) {
-        cudaFuncSetAttribute(k_region_unpermute<true, false, TT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
-        k_region_gather<true><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.overflow, reinterpret_cast<const uint32_t*>(B.rec), B.res);
-        k_region_unpermute<true, false, TT><<<tiles, TT, sm_unperm, st>>>(
-            rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
-    } else {
-        cudaFuncSetAttribute(k_region_unpermute<false, false, TT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm_unperm);
-        k_region_gather<false><<<static_cast<unsigned>(gblocks), 256, 0, st>>>(
-            rg, d_b, B.cursor, B.overflow, reinterpret_cast<const uint32_t*>(B.rec), B.res);
-        k_region_unpermute<false, false, TT><<<tiles, TT, sm_unperm, st>>>(
-            rg, d_b, B.overflow, B.runs, B.slot_of, B.res, base, o);
-    }
+    const unsigned gb = static_cast<unsigned>(gblocks);
+    const uint32_t* rec = reinterpret_cast<const uint32_t*>(B.rec);
+    if (g.philox)
+        k_region_gather<true, true><<<gb, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, rec, B.res);
+    else if (w1)
+        k_region_gather<true><<<gb, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, rec, B.res);
+    else
+        k_region_gather<false><<<gb, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, rec, B.res);
+    const bool bulk = rd_bulk();
+    if (g.philox)
+        bulk ? launch_unpermute<true, true, TT, true>(rg, d_b, B, base, o, tiles, sm_unperm, st)
+             : launch_unpermute<true, true, TT, false>(rg, d_b, B, base, o, tiles, sm_unperm, st);
+    else if (w1)
+        bulk ? launch_unpermute<true, false, TT, true>(rg, d_b, B, base, o, tiles, sm_unperm, st)
+             : launch_unpermute<true, false, TT, false>(rg, d_b, B, base, o, tiles, sm_unperm, st);
+    else
+        bulk ? launch_unpermute<false, false, TT, true>(rg, d_b, B, base, o, tiles, sm_unperm, st)
+             : launch_unpermute<false, false, TT, false>(rg, d_b, B, base, o, tiles, sm_unperm, st);
     return cudaGetLastError();
 }
 

@@ -365,9 +365,13 @@ def test_full_size_table_and_draws(P):
 
 # ---- region-ordered draw plan (table beyond L2) ---------------------------------------
 
-@pytest.mark.parametrize("chunk,shift", [(None, None), (3_000_001, None), (None, 22), (None, 19)])
-def test_region_plan_draws_bit_exact(P, chunk, shift, monkeypatch):
+@pytest.mark.parametrize("chunk,shift,rd", [(None, None, "1"), (3_000_001, None, "1"), (None, 22, "1"),
+                                            (None, 19, "1"), (None, None, "0"), (None, 19, "0")])
+def test_region_plan_draws_bit_exact(P, chunk, shift, rd, monkeypatch):
+    """rd: the unpermute's run staging -- bulk copies ("1", default) or the
+    warp-wide LDGSTS form ("0")."""
     import torch
+    monkeypatch.setenv("WRS_B200_RD_BULK", rd)
     if chunk:
         monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
     if shift:  # 64-MB regions (the default above 2^27 buckets) / many small regions
