@@ -334,7 +334,7 @@ __device__ __forceinline__ uint4 ld_table(const Bucket* b, uint64_t i, uint64_t 
 // copies; a padding slot holds a record whose draw index is REC_PAD, which
 // RC and the counting pass skip.
 constexpr uint32_t RUN_ALIGN = 4;
-constexpr uint32_t REC_PAD = 0xffffffffu;  // (draw indices within a chunk are < 2^31)
+constexpr uint32_t REC_PAD = 0xffffffffu;  // (draw indices within a chunk are < 2^32 - 1)
 __host__ __device__ inline uint32_t stage_slots(uint32_t nreg, uint32_t tile) {
     return tile + (RUN_ALIGN - 1) * nreg;
 }
@@ -1056,15 +1056,21 @@ struct RegionPlan {
 // Tile size by region count: a tile's runs (one per region) should average
 // tens of draws, or the slab writes and the unpermute's run reads fragment
 // (measured at n = 2^30, 512 regions: 8 draws per run with 4096-draw tiles).
-static int tile_threads_for(uint32_t nreg) {
+static int tile_threads_for(uint32_t nreg, bool counts) {
     if (const char* env = getenv("WRS_B200_TILE_THREADS")) {  // tests: force a tile size
         const int t = atoi(env);
         if (t == 256 || t == 512 || t == 1024) return t;
     }
-    return nreg <= 160 ? 256 : nreg <= 320 ? 512 : 1024;
+    // aggregated draws (no unpermute): 4096-draw tiles up to 160 regions
+    // (1e9 draws at n = 1e8: 11.52 ms vs 11.85 with 8192)
+    if (counts) return nreg <= 160 ? 256 : nreg <= 320 ? 512 : 1024;
+    // 8192-draw tiles up to 320 regions (with bulk-copied unpermute runs, 1e9
+    // draws: n = 1e8 8.08 -> 7.93 ms vs 4096-draw tiles, n = 2^28 8.66 -> 8.44,
+    // n = 2^30 10.84 vs 11.44; scripts/region_sweep.sh), 16384 above
+    return nreg <= 320 ? 512 : 1024;
 }
 
-static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
+static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk, bool counts = false) {
     RegionPlan p{};
     p.rg.g = g;
     p.rg.shift = region_shift(g.n);
@@ -1072,7 +1078,7 @@ static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk) {
     // expected draws per full region + ~20 sigma + two tiles of slack
     const double mu = static_cast<double>(chunk) *
                       (static_cast<double>(1ull << p.rg.shift) / static_cast<double>(g.n));
-    p.tt = tile_threads_for(p.rg.nreg);
+    p.tt = tile_threads_for(p.rg.nreg, counts);
     p.tile = static_cast<uint32_t>(p.tt * RS_ROWS);
     // + the runs' padding: up to RUN_ALIGN - 1 slots per (tile, region)
     const double pad = static_cast<double>(RUN_ALIGN - 1) * static_cast<double>((chunk + p.tile - 1) / p.tile);
@@ -1093,7 +1099,7 @@ static uint64_t region_chunk_max() {
     uint64_t chunk_max = 1ull << 30;  // draws per region pass
     if (const char* env = getenv("WRS_B200_DRAW_CHUNK")) {
         const unsigned long long v = strtoull(env, nullptr, 10);
-        if (v >= RS_TILE) chunk_max = v;
+        if (v >= RS_TILE) chunk_max = v < 3500000000ull ? v : 3500000000ull;
     }
     return chunk_max;
 }
@@ -1239,23 +1245,28 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
 }
 
 // Draws per region pass for a plain draw of cnt draws: every pass sweeps the
-// whole table once more (16 GB at n = 1e9), so big draws take passes of up to
-// 2^31 draws when the scratch (12 B per draw) fits comfortably in free device
-// memory, else 2^30 (or what WRS_B200_DRAW_CHUNK says).
+// whole table once more (16 GB at n = 1e9), so big draws take as few,
+// equal passes of up to kPassMax draws as keep the slab positions 32-bit and
+// the scratch (~12 B per draw) well inside free device memory; 2^30-draw
+// passes otherwise (or what WRS_B200_DRAW_CHUNK says).  1e10 draws: 3 passes
+// instead of 5 of 2^31.
 static uint64_t draw_chunk_for(const DrawGeom& g, uint64_t cnt, const SampleWorkspace* ws) {
     if (getenv("WRS_B200_DRAW_CHUNK")) return region_chunk_max();
-    uint64_t chunk = 1ull << 30;
-    if (cnt > chunk) {
-        size_t free_b = 0, total_b = 0;
-        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            const uint64_t big = cnt < (1ull << 31) ? cnt : (1ull << 31);
-            const RegionPlan p = plan_regions(g, big);
-            if (region_bytes(p, big, nullptr, nullptr) < 0.6 * (free_b + ws->bytes)) chunk = big;
-        } else {
-            cudaGetLastError();
-        }
+    constexpr uint64_t kBase = 1ull << 30, kPassMax = 3500000000ull;
+    if (cnt <= kBase) return kBase;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return kBase;
     }
-    return chunk;
+    for (uint64_t passes = (cnt + kPassMax - 1) / kPassMax;; ++passes) {
+        const uint64_t c = (cnt + passes - 1) / passes;
+        if (c <= kBase) return kBase;
+        const RegionPlan p = plan_regions(g, c);
+        if (p.rec_slots < (1ull << 32) - RC_SPAN &&
+            region_bytes(p, c, nullptr, nullptr) < 0.6 * (free_b + ws->bytes))
+            return c;
+    }
 }
 
 cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t seed,
@@ -1366,7 +1377,7 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
     RegionBuffers B{};
     int sm_scatter = 0;
     if (region) {
-        plan = plan_regions(g, chunk);
+        plan = plan_regions(g, chunk, true);
         if ((e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr))) != cudaSuccess) return e;
         region_bytes(plan, chunk, &B, ws->base);
         ws->overflow = B.overflow;

@@ -151,3 +151,28 @@ def test_draws_beyond_one_pass_bit_exact():
         for lo in (0, (1 << 30) - 50_000, k - 100_000):
             ref = P.sample_range(b, S.bucket_mean, 31, k, Wk, lo, lo + 100_000)
             assert np.array_equal(out[lo:lo + 100_000].cpu().numpy().view(np.uint32), ref), (Wk, lo)
+
+
+def test_draws_in_passes_beyond_2p31_bit_exact(monkeypatch):
+    """3.3e9 draws take ONE region pass (slab positions and draw indices up
+    to 2^32 - 1; draw_chunk_for): equal to the same draw in 2^30-draw passes,
+    and windows around 2^31 and at the end bit-exact against the oracle."""
+    import torch
+    import oracle
+    P = oracle.port()
+    n, k = 10_000_019, 3_300_000_001
+    W = wrs.Weights.generate("powerlaw", 0.5, n, 3)
+    S = wrs.Sampler.build(W, "psa", 1)
+    b = S.buckets()
+    one = torch.empty(k, dtype=torch.int32, device="cuda")
+    for Wk in (1, 5):
+        S.draw_device(17, k, Wk, one)
+        torch.cuda.synchronize()
+        for lo in (0, (1 << 31) - 50_000, k - 100_000):
+            ref = P.sample_range(b, S.bucket_mean, 17, k, Wk, lo, lo + 100_000)
+            assert np.array_equal(one[lo:lo + 100_000].cpu().numpy().view(np.uint32), ref), (Wk, lo)
+    monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(1 << 30))
+    four = torch.empty(k, dtype=torch.int32, device="cuda")
+    S.draw_device(17, k, 5, four)
+    torch.cuda.synchronize()
+    assert torch.equal(one, four)
