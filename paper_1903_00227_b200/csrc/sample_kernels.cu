@@ -1064,10 +1064,11 @@ static int tile_threads_for(uint32_t nreg, bool counts) {
     // aggregated draws (no unpermute): 4096-draw tiles up to 160 regions
     // (1e9 draws at n = 1e8: 11.52 ms vs 11.85 with 8192)
     if (counts) return nreg <= 160 ? 256 : nreg <= 320 ? 512 : 1024;
-    // 8192-draw tiles up to 320 regions (with bulk-copied unpermute runs, 1e9
-    // draws: n = 1e8 8.08 -> 7.93 ms vs 4096-draw tiles, n = 2^28 8.66 -> 8.44,
-    // n = 2^30 10.84 vs 11.44; scripts/region_sweep.sh), 16384 above
-    return nreg <= 320 ? 512 : 1024;
+    // 4096-draw tiles below 20 regions (1e9 draws at n = 2^24, 8 regions:
+    // 7.37 vs 7.73 ms with 8192), 8192 up to 320 (with bulk-copied unpermute
+    // runs: n = 1e8 8.08 -> 7.93 ms, n = 2^28 8.66 -> 8.44, n = 2^30 10.84 vs
+    // 11.44 with 4096; scripts/region_sweep.sh), 16384 above
+    return nreg < 20 ? 256 : nreg <= 320 ? 512 : 1024;
 }
 
 static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk, bool counts = false) {

@@ -18,9 +18,9 @@ first, last = [int(x) for x in re.search(r"launches (\d+)-(\d+)", t["source"]).g
 s = f"""# Round 2 evidence summary, final kernels (1 × B200, n = 1e8 uniform, k = 1e9 draws)
 
 Bench line: `profiles/{tag}_bench.json` (`python bench.py`, driver defaults;
-`TAG={tag} bash scripts/gpu_round2_profile.sh`). Peak = 6443.2 GB/s
-(`MEASURED_PEAKS.json`, measured copy bandwidth). Earlier round-2 states:
-`r02_summary.md` (round start), `r02b_*`, `r02c_*` (intermediate).
+`TAG={tag} bash scripts/gpu_round2_profile.sh`). Peak = {d['roofline']['peak']} GB/s
+(`MEASURED_PEAKS.json` of the pod the run was on, measured copy bandwidth). Earlier round-2 states:
+`r02_summary.md` (round start), `r02b_*`, `r02c_*`, `r02d_*` (intermediate).
 
 - step (rebuild + 1e9 draws, configs[1]): **{d['ms_per_step']:.2f} ms → {d['value']:.1f} G(items+samples)/s**
   (r01 11.91 ms → 92.3; round-2 start 11.51 → 95.6); clocks {d['clocks']}
