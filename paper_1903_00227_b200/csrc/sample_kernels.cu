@@ -367,8 +367,11 @@ constexpr int RC_SPAN = RC_ROWS * 256;  // slab positions per gather / count CTA
 #ifndef RS_MIN_CTAS
 #define RS_MIN_CTAS 6  // 256-thread CTAs per SM the register budget must allow (40 regs; 8.05 vs 8.16 ms at 5)
 #endif
-template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS, bool FULL = false>
-__global__ void __launch_bounds__(TT, RS_MIN_CTAS * 256 / TT)
+// ROWS: draws per thread (tile = TT * ROWS); 32 rows keep 256-thread CTAs
+// for 8192-draw tiles (4 CTAs per SM: 64 registers for the 32 buckets).
+template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS, bool FULL = false,
+          int ROWS = RS_ROWS>
+__global__ void __launch_bounds__(TT, (ROWS == RS_ROWS ? RS_MIN_CTAS * 256 : ROWS == 32 ? 1024 : 512) / TT)
 k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
                  unsigned* __restrict__ overflow, void* __restrict__ rec_out,
                  uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
@@ -385,14 +388,14 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     uint32_t* goff = fill + nreg;                          // [nreg] the runs' slab positions
     Rec* stage = reinterpret_cast<Rec*>(rs_smem + (((4 * nreg + 2) * 4 + 15) & ~15u));  // padded runs
     const uint64_t tile = static_cast<uint64_t>(tile0) + blockIdx.x;
-    const uint64_t tbase = tile * (TT * RS_ROWS);
+    const uint64_t tbase = tile * (TT * ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t i = threadIdx.x; i < nreg; i += TT) cnt[i] = 0;
     __syncthreads();
 
-    uint32_t bk[RS_ROWS];
+    uint32_t bk[ROWS];
     const uint32_t kc_left =
-        FULL ? (TT * RS_ROWS) : static_cast<uint32_t>(umin64(rg.kc - tbase, (TT * RS_ROWS)));
+        FULL ? (TT * ROWS) : static_cast<uint32_t>(umin64(rg.kc - tbase, (TT * ROWS)));
     const uint32_t n32 = static_cast<uint32_t>(rg.g.n);
     if (W1) {
         // single worker: counter of draw q is key + (2q + 1) G, and the rows of
@@ -402,11 +405,11 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         const uint64_t step = 2ull * TT * kGolden;
         if constexpr (PHX) {
 #pragma unroll
-            for (int r = 0; r < RS_ROWS; ++r)
+            for (int r = 0; r < ROWS; ++r)
                 bk[r] = philox_bucket(rg.g, rg.q0 + tbase + r * TT + threadIdx.x);
         } else {
 #pragma unroll
-            for (int r = 0; r < RS_ROWS; ++r) {
+            for (int r = 0; r < ROWS; ++r) {
                 bk[r] = mulhi_n32(mix64(c1), n32);
                 c1 += step;
             }
@@ -415,7 +418,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         DrawCursor<W1> cur;
         cur.init(rg.g, rg.q0 + tbase + threadIdx.x);
 #pragma unroll
-        for (int r = 0; r < RS_ROWS; ++r) {
+        for (int r = 0; r < ROWS; ++r) {
             const uint32_t e = r * TT + threadIdx.x;
             bk[r] = e < kc_left
                         ? static_cast<uint32_t>(bucket_of_ctr(rg.g, cur.ctr1(rg.g, rg.q0 + tbase + e)))
@@ -423,7 +426,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         }
     }
 #pragma unroll
-    for (int r = 0; r < RS_ROWS; ++r) {
+    for (int r = 0; r < ROWS; ++r) {
         const uint32_t e = r * TT + threadIdx.x;
         if (e < kc_left) atomicAdd(&cnt[bk[r] >> rg.shift], 1u);
     }
@@ -479,7 +482,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     }
     const uint32_t t32 = static_cast<uint32_t>(tbase);
 #pragma unroll
-    for (int r = 0; r < RS_ROWS; ++r) {
+    for (int r = 0; r < ROWS; ++r) {
         const uint32_t e = r * TT + threadIdx.x;
         if (e < kc_left) {
             const uint32_t slot = atomicAdd(&fill[bk[r] >> rg.shift], 1u);
@@ -1064,11 +1067,11 @@ static int tile_threads_for(uint32_t nreg, bool counts) {
     // aggregated draws (no unpermute): 4096-draw tiles up to 160 regions
     // (1e9 draws at n = 1e8: 11.52 ms vs 11.85 with 8192)
     if (counts) return nreg <= 160 ? 256 : nreg <= 320 ? 512 : 1024;
-    // 4096-draw tiles below 20 regions (1e9 draws at n = 2^24, 8 regions:
-    // 7.37 vs 7.73 ms with 8192), 8192 up to 320 (with bulk-copied unpermute
-    // runs: n = 1e8 8.08 -> 7.93 ms, n = 2^28 8.66 -> 8.44, n = 2^30 10.84 vs
-    // 11.44 with 4096; scripts/region_sweep.sh), 16384 above
-    return nreg < 20 ? 256 : nreg <= 320 ? 512 : 1024;
+    // 8192-draw tiles up to 320 regions, 16384 above (bulk-copied unpermute
+    // runs, 32-row scatter; 1e9 draws with 4096 / 8192 / 16384-draw tiles:
+    // n = 2e7 7.40 / 7.38 / 7.64 ms, 1e8 7.92 / 7.75 / 7.89, 2^28 8.52 / 8.25 /
+    // 8.36, 2^30 11.34 / 10.25 / 10.45; scripts/tt_rows_sweep.sh)
+    return nreg <= 320 ? 512 : 1024;
 }
 
 static RegionPlan plan_regions(const DrawGeom& g, uint64_t chunk, bool counts = false) {
@@ -1162,24 +1165,40 @@ void SampleWorkspace::release() {
 
 // RB over a chunk: the full tiles in one launch, the partial last tile (if
 // any) in a one-CTA launch of the bounds-checked variant.
-template <bool W1, bool ORDER, bool PHX, int TT>
+template <bool W1, bool ORDER, bool PHX, int TT, int ROWS = RS_ROWS>
 static void launch_scatter(const RegionGeom& rg, const RegionBuffers& B, int smem, cudaStream_t s) {
-    const uint64_t full = rg.kc / (static_cast<uint64_t>(TT) * RS_ROWS);
+    const uint64_t full = rg.kc / (static_cast<uint64_t>(TT) * ROWS);
     if (full) {
-        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, true>,
+        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, true, ROWS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, true>,
+        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, true, ROWS>,
                              cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        k_region_scatter<W1, ORDER, PHX, TT, true><<<static_cast<unsigned>(full), TT, smem, s>>>(
+        k_region_scatter<W1, ORDER, PHX, TT, true, ROWS><<<static_cast<unsigned>(full), TT, smem, s>>>(
             rg, 0u, B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
     }
     if (rg.ntiles > full) {
-        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, false>,
+        cudaFuncSetAttribute(k_region_scatter<W1, ORDER, PHX, TT, false, ROWS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_region_scatter<W1, ORDER, PHX, TT, false><<<1, TT, smem, s>>>(
+        k_region_scatter<W1, ORDER, PHX, TT, false, ROWS><<<1, TT, smem, s>>>(
             rg, static_cast<uint32_t>(full), B.cursor, B.overflow, B.rec, B.slot_of, B.runs);
     }
+}
+// The scatter of a TT * 16-draw tile as TT / 2 threads x 32 rows (default)
+// or TT / 4 x 64 / TT x 16 (WRS_B200_SCATTER_ROWS=64 / 16, A/B): fewer,
+// longer-lived threads per tile (1e9 draws, n = 1e8: scatter 1.88 -> 1.65 ms
+// at 8192-draw tiles).
+static int scatter_rows() {
+    const char* e = getenv("WRS_B200_SCATTER_ROWS");
+    const int r = e ? atoi(e) : 32;
+    return r == 16 || r == 64 ? r : 32;
+}
+template <bool W1, bool ORDER, bool PHX, int TT>
+static void launch_scatter_tt(const RegionGeom& rg, const RegionBuffers& B, int smem, cudaStream_t s) {
+    const int rows = scatter_rows();
+    if (rows == 32) return launch_scatter<W1, ORDER, PHX, TT / 2, 32>(rg, B, smem, s);
+    if (rows == 64) return launch_scatter<W1, ORDER, PHX, TT / 4, 64>(rg, B, smem, s);
+    launch_scatter<W1, ORDER, PHX, TT>(rg, B, smem, s);
 }
 
 // RD staging: one bulk copy per run (default) or warp-wide 16-B LDGSTS
@@ -1215,11 +1234,11 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
     const unsigned tiles = static_cast<unsigned>(rg.ntiles);
     const uint64_t gblocks = (plan.rec_slots + RC_SPAN - 1) / RC_SPAN;
     if (g.philox)
-        launch_scatter<true, true, true, TT>(rg, B, sm_scatter, ss);
+        launch_scatter_tt<true, true, true, TT>(rg, B, sm_scatter, ss);
     else if (w1)
-        launch_scatter<true, true, false, TT>(rg, B, sm_scatter, ss);
+        launch_scatter_tt<true, true, false, TT>(rg, B, sm_scatter, ss);
     else
-        launch_scatter<false, true, false, TT>(rg, B, sm_scatter, ss);
+        launch_scatter_tt<false, true, false, TT>(rg, B, sm_scatter, ss);
     if (on_side) {
         if ((e = cudaEventRecord(side_ev, side)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
@@ -1324,6 +1343,8 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
 template <bool W1>
 static cudaError_t count_scatter(int tt, const RegionGeom& rg, const RegionBuffers& B,
                                  int sm_scatter, cudaStream_t st) {
+    // (16 rows per thread: the 32-row form measured slower here, 11.68 vs
+    // 11.55 ms per 1e9 aggregated draws at n = 1e8)
     switch (tt) {
         case 256: launch_scatter<W1, false, false, 256>(rg, B, sm_scatter, st); break;
         case 512: launch_scatter<W1, false, false, 512>(rg, B, sm_scatter, st); break;

@@ -365,13 +365,17 @@ def test_full_size_table_and_draws(P):
 
 # ---- region-ordered draw plan (table beyond L2) ---------------------------------------
 
-@pytest.mark.parametrize("chunk,shift,rd", [(None, None, "1"), (3_000_001, None, "1"), (None, 22, "1"),
-                                            (None, 19, "1"), (None, None, "0"), (None, 19, "0")])
-def test_region_plan_draws_bit_exact(P, chunk, shift, rd, monkeypatch):
+@pytest.mark.parametrize("chunk,shift,rd,rows", [
+    (None, None, "1", "32"), (3_000_001, None, "1", "32"), (None, 22, "1", "32"),
+    (None, 19, "1", "32"), (None, None, "0", "32"), (None, 19, "0", "32"),
+    (None, None, "1", "16"), (3_000_001, 19, "1", "64")])
+def test_region_plan_draws_bit_exact(P, chunk, shift, rd, rows, monkeypatch):
     """rd: the unpermute's run staging -- bulk copies ("1", default) or the
-    warp-wide LDGSTS form ("0")."""
+    warp-wide LDGSTS form ("0"); rows: draws per scatter thread (32 default;
+    16 / 64 the other scatter forms of the same tile)."""
     import torch
     monkeypatch.setenv("WRS_B200_RD_BULK", rd)
+    monkeypatch.setenv("WRS_B200_SCATTER_ROWS", rows)
     if chunk:
         monkeypatch.setenv("WRS_B200_DRAW_CHUNK", str(chunk))
     if shift:  # 64-MB regions (the default above 2^27 buckets) / many small regions
