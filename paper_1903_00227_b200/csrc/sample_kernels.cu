@@ -22,12 +22,16 @@
 //           a tile-local counting sort into per-region slabs (space claimed by
 //           atomics), the gathers then sweep the table region by region so
 //           every line is fetched from HBM about once, and a final pass puts
-//           the answers back in output order.  Traffic per draw: 8 B record
-//           write + 8 B read + 2 B slot write + 2 B read + 4 B result write +
-//           4 B read + 4 B output write, plus 16n B of table per pass.
-//     RB  k_region_scatter   (q, bucket) records, runs per (tile, region)
-//     RC  k_region_gather    coin flip + bucket gather, region by region
-//     RD  k_region_unpermute out[q] = result at the slot RB gave draw q
+//           the answers back in output order.  Traffic per draw: 4 B record
+//           (the draw's index) write + 4 B read + 2 B slot write + 2 B read +
+//           4 B result write + 4 B read + 4 B output write, plus 16n B of
+//           table per pass (passes of up to 3.5e9 draws).
+//     RB  k_region_scatter   draw-index records, runs per (tile, region),
+//                            each run one bulk copy to its slab
+//     RC  k_region_gather    bucket + coin recomputed, bucket gather, region
+//                            by region
+//     RD  k_region_unpermute out[q] = result at the slot RB gave draw q; each
+//                            of the tile's runs staged with one bulk copy
 //   Aggregated draws reuse RB and count instead of writing (k_region_count,
 //   k_count_fold, k_compact_*); k_two_level_sample routes two-level draws;
 //   the Philox mode is a compile-time variant of every draw kernel.
