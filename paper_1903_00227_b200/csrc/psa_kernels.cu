@@ -184,7 +184,10 @@ k_total(const double* __restrict__ w, uint64_t n, int D, double* node_val,
 #endif
 constexpr int K1_THREADS = K1_THREADS_DEF;
 constexpr int K1_WARPS = K1_THREADS / 32;
-constexpr int K1_ROWS = 16;
+#ifndef K1_ROWS_DEF
+#define K1_ROWS_DEF 16
+#endif
+constexpr int K1_ROWS = K1_ROWS_DEF;
 constexpr int K1_TILE = K1_THREADS * K1_ROWS;  // 4096
 constexpr int K1_SLOTS = K1_ROWS * (K1_THREADS / 32);  // (row, warp) cells
 constexpr int K1_CPL = K1_SLOTS / 32;                  // cells per lane in the tile scan
