@@ -39,10 +39,10 @@ UNIT = "G(items+samples)/s"
 BUILD_BYTES_PER_ITEM = 72   # SURVEY.md §8(d) minus K0 (W comes with the weights, as the
                             # reference's WeightTable): K1 20 + K2 24 + K4 28
 SAMPLE_BYTES_PER_DRAW = 36  # one 32-B sector gather + one 4-B index store
-KERNELS_PER_STEP = 11       # build: k_partition, k_scan_blocks x2, k_scan_carry, k_split,
-                            # k_pack, k_assemble; draw: k_region_scatter (full tiles + the
-                            # partial last tile: 1e9 is not a multiple of 4096), _gather,
-                            # _unpermute
+KERNELS_PER_STEP = 10       # build: k_reset_scalars, k_partition_direct, k_carry_ckpt (K2
+                            # fused), k_split, k_pack, k_assemble; draw: k_region_scatter
+                            # (full tiles + the partial last tile: 1e9 is not a multiple of
+                            # 8192), _gather, _unpermute (profiles/r02f_launch_list.txt)
 
 
 def parse():
