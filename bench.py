@@ -498,6 +498,20 @@ def config1(ctx, weak_world: int):
     return res
 
 
+def draw_launches(k: int) -> int:
+    """Draw kernels of one k-draw call (region plan, 8192-draw tiles): per
+    region pass a scatter (+ a one-CTA launch for a partial last tile), a
+    gather and an unpermute; passes as sample_kernels.cu draw_chunk_for makes
+    them (equal passes of up to 3.5e9 draws beyond 2^30)."""
+    if k <= 1 << 30:
+        passes = [k]
+    else:
+        p = -(-k // 3_500_000_000)
+        c = -(-k // p)
+        passes = [c] * (p - 1) + [k - c * (p - 1)]
+    return sum(3 + (1 if c % 8192 else 0) for c in passes)
+
+
 def config2(ctx):
     """BASELINE configs[2]: n = 1e9 power-law s = 1 weights (the reference
     generator: (i+1)^-1 dealt by its Fisher-Yates, seed 42), sharded
@@ -555,7 +569,7 @@ def config2(ctx):
         "per_rank": {"items": hi - lo, "draws_max": int(counts.max()), "draws_min": int(counts.min()),
                      "build_ms_max": build_ms, "draw_ms_max": draw_ms,
                      "build": build, "draw_roofline": draw_roof},
-        "gpu_launches": (KERNELS_PER_STEP + 1) * args.steps,
+        "gpu_launches": (6 + draw_launches(int(counts.max())) + (1 if nccl else 0)) * args.steps,
         "clocks": clocks.summary(),
     }
     del out
