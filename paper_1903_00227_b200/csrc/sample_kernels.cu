@@ -188,6 +188,15 @@ __device__ __forceinline__ uint32_t philox_bucket(const DrawGeom& g, uint64_t q)
     philox_words(g, q, o);
     return mulhi_n32((static_cast<uint64_t>(o[1]) << 32) | o[0], static_cast<uint32_t>(g.n));
 }
+// bucket and coin of draw q from ONE Philox evaluation (the words feed both)
+__device__ __forceinline__ void philox_draw(const DrawGeom& g, uint64_t q, uint32_t& bucket,
+                                            double& coin) {
+    uint32_t o[4];
+    philox_words(g, q, o);
+    bucket = mulhi_n32((static_cast<uint64_t>(o[1]) << 32) | o[0], static_cast<uint32_t>(g.n));
+    const uint64_t r = (static_cast<uint64_t>(o[3]) << 32) | o[2];
+    coin = (static_cast<double>(r >> 11) * 0x1.0p-53) * g.wn;
+}
 __device__ __forceinline__ double philox_coin(const DrawGeom& g, uint64_t q) {
     uint32_t o[4];
     philox_words(g, q, o);
@@ -233,8 +242,9 @@ k_sample(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint64_t q_
             x[u] = 0.0;
             if (q < q_end) {
                 if constexpr (PHX) {
-                    bidx[u] = philox_bucket(g, q);
-                    x[u] = philox_coin(g, q);
+                    uint32_t bb;
+                    philox_draw(g, q, bb, x[u]);
+                    bidx[u] = bb;
                     continue;
                 }
                 const uint64_t c1 = cur.ctr1(g, q);
@@ -573,6 +583,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         return kc.get(rg.g, w) + (2 * m + 1) * kGolden;
     };
     uint32_t r[RC_ROWS];
+    double xph[RC_ROWS];  // Philox mode: the coins, from the same evaluation as the buckets
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
@@ -589,7 +600,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         if (r[u] != REC_PAD) {
             uint32_t bi;
             if constexpr (PHX)
-                bi = philox_bucket(rg.g, rg.q0 + r[u]);
+                philox_draw(rg.g, rg.q0 + r[u], bi, xph[u]);
             else
                 bi = mulhi_n32(mix64(ctr1(r[u])), n32);
             WRS_CHECK(bi < rg.g.n);
@@ -606,7 +617,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         if (r[u] != REC_PAD) {  // (positions past valid_end read as padding)
             double x;
             if constexpr (PHX)
-                x = philox_coin(rg.g, rg.q0 + r[u]);
+                x = xph[u];
             else
                 x = coin_of_ctr(rg.g, ctr1(r[u]));
             st_stream(res + p, pick(bk, x), pf);
@@ -636,8 +647,10 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
         for (uint32_t e = threadIdx.x; e < tcount; e += TT) {
             const uint64_t q = rg.q0 + tbase + e;
             if constexpr (PHX) {
-                out[tbase + e] = pick(ld_bucket(b, philox_bucket(rg.g, q)), philox_coin(rg.g, q)) +
-                                 out_base;
+                uint32_t bb;
+                double xx;
+                philox_draw(rg.g, q, bb, xx);
+                out[tbase + e] = pick(ld_bucket(b, bb), xx) + out_base;
                 continue;
             }
             const uint64_t c1 = cur.ctr1(rg.g, q);
@@ -812,8 +825,7 @@ k_count_direct(const Bucket* __restrict__ b, DrawGeom g, uint64_t q_begin, uint6
         uint32_t bi;
         double x;
         if constexpr (PHX) {
-            bi = philox_bucket(g, q);
-            x = philox_coin(g, q);
+            philox_draw(g, q, bi, x);
         } else {
             const uint64_t c1 = cur.ctr1(g, q);
             bi = static_cast<uint32_t>(bucket_of_ctr(g, c1));
