@@ -389,10 +389,9 @@ __global__ void __launch_bounds__(TT, (ROWS == RS_ROWS ? RS_MIN_CTAS * 256 : ROW
 k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
                  unsigned* __restrict__ overflow, void* __restrict__ rec_out,
                  uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
-    // plain draws: 4-B records, the draw's index in the chunk (the gather
-    // recomputes its bucket and coin from the counter-based stream);
-    // aggregated draws: {draw index, bucket}
-    using Rec = std::conditional_t<ORDER, uint32_t, uint2>;
+    // 4-B records, the draw's index in the chunk (the gather / counting pass
+    // recomputes its bucket and coin from the counter-based stream)
+    using Rec = uint32_t;
     Rec* const rec = static_cast<Rec*>(rec_out);
     extern __shared__ __align__(16) unsigned char rs_smem[];
     const uint32_t nreg = rg.nreg;
@@ -488,11 +487,7 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
     // from the slots the draws take below)
     for (uint32_t reg = threadIdx.x; reg < nreg; reg += TT) {
         if (ORDER) runs[tile * nreg + reg] = RunInfo{goff[reg], start[reg + 1]};
-        for (uint32_t i = start[reg] + cnt[reg]; i < start[reg + 1]; ++i)
-            if constexpr (ORDER)
-                stage[i] = REC_PAD;
-            else
-                stage[i] = make_uint2(REC_PAD, 0u);
+        for (uint32_t i = start[reg] + cnt[reg]; i < start[reg + 1]; ++i) stage[i] = REC_PAD;
     }
     const uint32_t t32 = static_cast<uint32_t>(tbase);
 #pragma unroll
@@ -500,12 +495,8 @@ k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
         const uint32_t e = r * TT + threadIdx.x;
         if (e < kc_left) {
             const uint32_t slot = atomicAdd(&fill[bk[r] >> rg.shift], 1u);
-            if constexpr (ORDER) {
-                stage[slot] = t32 + e;
-                slot_of[tbase + e] = static_cast<uint16_t>(slot);
-            } else {
-                stage[slot] = make_uint2(t32 + e, bk[r]);
-            }
+            stage[slot] = t32 + e;
+            if constexpr (ORDER) slot_of[tbase + e] = static_cast<uint16_t>(slot);
         }
     }
     // (no early exit on overflow: an overflowed run is written to the start
@@ -762,7 +753,7 @@ __device__ __forceinline__ void count_hit(uint32_t* hits, uint64_t n, uint32_t b
 template <bool W1, bool PHX = false>
 __global__ void __launch_bounds__(256, RC_MIN_CTAS)
 k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __restrict__ cursor,
-               const unsigned* __restrict__ overflow, const uint2* __restrict__ rec,
+               const unsigned* __restrict__ overflow, const uint32_t* __restrict__ rec,
                uint32_t* __restrict__ hits) {
     if (*overflow) return;  // k_count_direct<.., true> recounts the chunk
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * RC_SPAN;
@@ -771,41 +762,52 @@ k_region_count(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __re
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     KeyCache kc;
     const uint64_t key0 = rng_derive(rg.g.base_key, 0);
-    uint2 r[RC_ROWS];
+    const uint32_t n32 = static_cast<uint32_t>(rg.g.n);
+    // records are draw indices, as for the plain gather: bucket and coin are
+    // recomputed here (one counter per draw, kept for the coin)
+    uint32_t r[RC_ROWS], bi[RC_ROWS];
+    double x[RC_ROWS];
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const uint64_t p = p0 + u * 256 + threadIdx.x;
-        r[u] = p < valid_end ? ld_stream(rec + p, pf) : make_uint2(REC_PAD, 0);
+        r[u] = p < valid_end ? ld_stream(rec + p, pf) : REC_PAD;
     }
     __shared__ uint4 bk_s[RC_ROWS * 256];
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
-        if (r[u].x != REC_PAD)  // (padding records: no draw)
+        bi[u] = 0;
+        x[u] = 0.0;
+        if (r[u] != REC_PAD) {  // (padding records: no draw)
+            const uint64_t q = rg.q0 + r[u];
+            if constexpr (PHX) {
+                philox_draw(rg.g, q, bi[u], x[u]);
+            } else {
+                uint64_t c1;
+                if (W1) {
+                    c1 = key0 + (2 * q + 1) * kGolden;
+                } else {
+                    uint32_t w;
+                    uint64_t m;
+                    locate(rg.g, q, w, m);
+                    c1 = kc.get(rg.g, w) + (2 * m + 1) * kGolden;
+                }
+                bi[u] = mulhi_n32(mix64(c1), n32);
+                x[u] = coin_of_ctr(rg.g, c1);
+            }
+            WRS_CHECK(bi[u] < rg.g.n);
             asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
-                         ::"r"(s), "l"(b + r[u].y), "l"(pl) : "memory");
+                         ::"r"(s), "l"(b + bi[u]), "l"(pl) : "memory");
+        }
     }
     cp_async_commit();
     cp_async_wait<0>();
 #pragma unroll
     for (int u = 0; u < RC_ROWS; ++u) {
-        const uint64_t p = p0 + u * 256 + threadIdx.x;
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
-        if (p < valid_end && r[u].x != REC_PAD) {
-            double x;
-            if (W1) {
-                if constexpr (PHX)
-                    x = philox_coin(rg.g, rg.q0 + r[u].x);
-                else
-                    x = coin_of_ctr(rg.g, key0 + (2 * (rg.q0 + r[u].x) + 1) * kGolden);
-            } else {
-                uint32_t w;
-                uint64_t m;
-                locate(rg.g, rg.q0 + r[u].x, w, m);
-                x = draw_coin(rg.g, kc.get(rg.g, w), m);
-            }
+        if (r[u] != REC_PAD) {
             const double share = __hiloint2double(static_cast<int>(bk.y), static_cast<int>(bk.x));
-            count_hit(hits, rg.g.n, r[u].y, x >= share);  // ia[x >= share]
+            count_hit(hits, rg.g.n, bi[u], x[u] >= share);  // ia[x >= share]
         }
     }
 }
@@ -1080,9 +1082,9 @@ static int tile_threads_for(uint32_t nreg, bool counts) {
         const int t = atoi(env);
         if (t == 256 || t == 512 || t == 1024) return t;
     }
-    // aggregated draws (no unpermute): 4096-draw tiles up to 160 regions
-    // (1e9 draws at n = 1e8: 11.52 ms vs 11.85 with 8192)
-    if (counts) return nreg <= 160 ? 256 : nreg <= 320 ? 512 : 1024;
+    // (aggregated draws, 4-B records and the 32-row scatter: 1e9 draws at
+    // n = 1e8 with 4096 / 8192 / 16384-draw tiles 10.77 / 10.70 / 10.88 ms)
+    (void)counts;
     // 8192-draw tiles up to 320 regions, 16384 above (bulk-copied unpermute
     // runs, 32-row scatter; 1e9 draws with 4096 / 8192 / 16384-draw tiles:
     // n = 2e7 7.40 / 7.38 / 7.64 ms, 1e8 7.92 / 7.75 / 7.89, 2^28 8.52 / 8.25 /
@@ -1125,7 +1127,7 @@ static uint64_t region_chunk_max() {
 }
 
 struct RegionBuffers {
-    uint2* rec;
+    uint32_t* rec;  // draw-index records
     uint32_t* res;
     uint16_t* slot_of;
     RunInfo* runs;
@@ -1149,13 +1151,13 @@ static uint64_t region_bytes(const RegionPlan& p, uint64_t chunk, RegionBuffers*
         off += (bytes + 255) & ~uint64_t(255);
         return static_cast<char*>(base) + o;
     };
-    char* rec = take(p.rec_slots * sizeof(uint2));
+    char* rec = take(p.rec_slots * sizeof(uint32_t));
     char* res = take(p.rec_slots * sizeof(uint32_t));
     char* slot = take(chunk * sizeof(uint16_t));
     char* runs = take(ntiles * p.rg.nreg * sizeof(RunInfo));
     char* cur = take((2 * p.rg.nreg + 1) * 4 + 4);
     if (b) {
-        b->rec = reinterpret_cast<uint2*>(rec);
+        b->rec = reinterpret_cast<uint32_t*>(rec);
         b->res = reinterpret_cast<uint32_t*>(res);
         b->slot_of = reinterpret_cast<uint16_t*>(slot);
         b->runs = reinterpret_cast<RunInfo*>(runs);
@@ -1260,7 +1262,7 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
         if ((e = cudaStreamWaitEvent(st, side_ev, 0)) != cudaSuccess) return e;
     }
     const unsigned gb = static_cast<unsigned>(gblocks);
-    const uint32_t* rec = reinterpret_cast<const uint32_t*>(B.rec);
+    const uint32_t* rec = B.rec;
     if (g.philox)
         k_region_gather<true, true><<<gb, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, rec, B.res);
     else if (w1)
@@ -1359,12 +1361,12 @@ cudaError_t launch_sample(const Bucket* d_b, uint64_t n, double wn, uint64_t see
 template <bool W1>
 static cudaError_t count_scatter(int tt, const RegionGeom& rg, const RegionBuffers& B,
                                  int sm_scatter, cudaStream_t st) {
-    // (16 rows per thread: the 32-row form measured slower here, 11.68 vs
-    // 11.55 ms per 1e9 aggregated draws at n = 1e8)
+    // (32 rows per scatter thread, as for plain draws: 10.89 -> 10.77 ms per
+    // 1e9 aggregated draws at n = 1e8 with 4-B records)
     switch (tt) {
-        case 256: launch_scatter<W1, false, false, 256>(rg, B, sm_scatter, st); break;
-        case 512: launch_scatter<W1, false, false, 512>(rg, B, sm_scatter, st); break;
-        default: launch_scatter<W1, false, false, 1024>(rg, B, sm_scatter, st); break;
+        case 256: launch_scatter_tt<W1, false, false, 256>(rg, B, sm_scatter, st); break;
+        case 512: launch_scatter_tt<W1, false, false, 512>(rg, B, sm_scatter, st); break;
+        default: launch_scatter_tt<W1, false, false, 1024>(rg, B, sm_scatter, st); break;
     }
     return cudaGetLastError();
 }
@@ -1419,7 +1421,7 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
         if ((e = ws->reserve(region_bytes(plan, chunk, nullptr, nullptr))) != cudaSuccess) return e;
         region_bytes(plan, chunk, &B, ws->base);
         ws->overflow = B.overflow;
-        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg, plan.tile, sizeof(uint2)));
+        sm_scatter = static_cast<int>(scatter_smem_bytes(plan.rg.nreg, plan.tile, sizeof(uint32_t)));
     }
     const unsigned fold_blocks = static_cast<unsigned>(
         umin64((n + 255) / 256, static_cast<uint64_t>(sm_count()) * 8));
@@ -1437,14 +1439,14 @@ cudaError_t launch_count(const Bucket* d_b, uint64_t n, double wn, uint64_t seed
                 umin64((rg.kc + span - 1) / span, static_cast<uint64_t>(sm_count()) * 8));
             if (w1) {
                 if ((e = count_scatter<true>(plan.tt, rg, B, sm_scatter, st)) != cudaSuccess) return e;
-                k_region_count<true><<<gblocks, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, B.rec,
-                                                              cw->hits);
+                k_region_count<true><<<gblocks, 256, 0, st>>>(
+                    rg, d_b, B.cursor, B.overflow, B.rec, cw->hits);
                 k_count_direct<true, true><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1, B.overflow,
                                                                            cw->hits);
             } else {
                 if ((e = count_scatter<false>(plan.tt, rg, B, sm_scatter, st)) != cudaSuccess) return e;
-                k_region_count<false><<<gblocks, 256, 0, st>>>(rg, d_b, B.cursor, B.overflow, B.rec,
-                                                               cw->hits);
+                k_region_count<false><<<gblocks, 256, 0, st>>>(
+                    rg, d_b, B.cursor, B.overflow, B.rec, cw->hits);
                 k_count_direct<false, true><<<dblocks, K5_THREADS, 0, st>>>(d_b, g, c0, c1,
                                                                             B.overflow, cw->hits);
             }
