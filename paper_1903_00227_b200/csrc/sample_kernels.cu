@@ -1285,7 +1285,7 @@ static cudaError_t region_pass(const RegionPlan& plan, const RegionGeom& rg, con
 // Draws per region pass for a plain draw of cnt draws: every pass sweeps the
 // whole table once more (16 GB at n = 1e9), so big draws take as few,
 // equal passes of up to kPassMax draws as keep the slab positions 32-bit and
-// the scratch (~12 B per draw) well inside free device memory; 2^30-draw
+// the scratch (~10 B per draw) well inside free device memory; 2^30-draw
 // passes otherwise (or what WRS_B200_DRAW_CHUNK says).  1e10 draws: 3 passes
 // instead of 5 of 2^31.
 static uint64_t draw_chunk_for(const DrawGeom& g, uint64_t cnt, const SampleWorkspace* ws) {
