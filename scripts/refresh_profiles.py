@@ -75,9 +75,13 @@ json.dump({"draw_bytes_per_sample": round(dt * 1e9 / k, 2),
           open(os.path.join(P, "traffic.json"), "w"), indent=1)
 
 rep = os.path.join(G, f"prof_{tag}.ncu-rep")
-if os.path.exists(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+raw_csv = os.path.join(G, f"prof_{tag}_raw.csv")  # exported on the box when the report is too big to bring back
+if os.path.exists(rep) or os.path.exists(raw_csv):
+    if os.path.exists(rep):
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+    else:
+        raw = open(raw_csv).read()
     open("/tmp/raw_prof.csv", "w").write(raw)
     summ = run(os.path.join(HERE, "scripts", "ncu_summary.py"), "/tmp/raw_prof.csv").splitlines()
     out, seen, i = [f"# ncu --set full --clock-control none, one launch of each kernel of a bench "
