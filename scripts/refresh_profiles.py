@@ -87,7 +87,7 @@ if os.path.exists(rep) or os.path.exists(raw_csv):
     out, seen, i = [f"# ncu --set full --clock-control none, one launch of each kernel of a bench "
                     f"step (n=1e8, k=1e9), 1x B200",
                     f"# command: TAG={tag} bash scripts/gpu_round2_profile.sh (report "
-                    f"gpurun_out/prof_{tag}.ncu-rep)"], set(), 0
+                    f"gpurun_out/prof_{tag}.ncu-rep; its raw page: profiles/{tag}_ncu_raw.csv)"], set(), 0
     while i < len(summ):
         blk = [summ[i]]
         if i + 1 < len(summ) and summ[i + 1].startswith("    "):
