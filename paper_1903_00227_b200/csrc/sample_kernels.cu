@@ -372,6 +372,9 @@ __host__ __device__ inline size_t scatter_smem_bytes(uint32_t nreg, uint32_t til
 #define RC_ROWS 12  // records per gather / count thread (8.02 vs 8.06 ms at 8, 1e9 draws, n = 1e8)
 #endif
 constexpr int RC_SPAN = RC_ROWS * 256;  // slab positions per gather / count CTA
+#ifndef RC_COIN_EARLY
+#define RC_COIN_EARLY 1  // gather: coins computed while the bucket rows are in flight
+#endif
 #ifndef RC_MIN_CTAS
 #define RC_MIN_CTAS 4  // gather / count CTAs per SM (48 KB of bucket rows each)
 #endif
@@ -590,13 +593,20 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(&bk_s[u * 256 + threadIdx.x]));
         if (r[u] != REC_PAD) {
             uint32_t bi;
-            if constexpr (PHX)
+            uint64_t c1 = 0;
+            if constexpr (PHX) {
                 philox_draw(rg.g, rg.q0 + r[u], bi, xph[u]);
-            else
-                bi = mulhi_n32(mix64(ctr1(r[u])), n32);
+            } else {
+                c1 = ctr1(r[u]);
+                bi = mulhi_n32(mix64(c1), n32);
+            }
             WRS_CHECK(bi < rg.g.n);
             asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n"
                          ::"r"(s), "l"(b + bi), "l"(pl) : "memory");
+#if RC_COIN_EARLY
+            // the coin while the row is in flight (not after the wait)
+            if constexpr (!PHX) xph[u] = coin_of_ctr(rg.g, c1);
+#endif
         }
     }
     cp_async_commit();
@@ -607,7 +617,7 @@ k_region_gather(RegionGeom rg, const Bucket* __restrict__ b, const uint32_t* __r
         const uint4 bk = bk_s[u * 256 + threadIdx.x];
         if (r[u] != REC_PAD) {  // (positions past valid_end read as padding)
             double x;
-            if constexpr (PHX)
+            if constexpr (PHX || RC_COIN_EARLY)
                 x = xph[u];
             else
                 x = coin_of_ctr(rg.g, ctr1(r[u]));
@@ -690,7 +700,8 @@ k_region_unpermute(RegionGeom rg, const Bucket* __restrict__ b,
     // staging, so every element of the tile is in flight at once.  Warp w
     // owns runs w, w + WARPS, ...; their descriptors are loaded by one lane
     // each, all at once, and handed round by shuffles.
-    for (uint32_t r0 = warp; r0 < (BULK ? 0u : rg.nreg); r0 += 32 * WARPS) {
+    const uint32_t ldgsts_regions = BULK ? 0u : rg.nreg;  // (the bulk form staged above)
+    for (uint32_t r0 = warp; r0 < ldgsts_regions; r0 += 32 * WARPS) {
         const uint32_t reg = r0 + lane * WARPS;
         uint32_t goff = 0, loc = 0, end = 0;
         if (reg < rg.nreg) {
