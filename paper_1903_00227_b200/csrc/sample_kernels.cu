@@ -1072,10 +1072,11 @@ bool use_region_plan(uint64_t n, uint64_t k) {
         if (env[0] == 'd') return false;
         if (env[0] == 'r') return nreg <= RS_MAX_REGIONS;
     }
-    // table beyond ~136 MB (measured crossover on B200, scripts/plan_crossover.py:
-    // direct 8.9 vs region 9.5 ms per 1e9 draws at 128 MB, 11.1 vs 9.4 at 160 MB)
-    // and enough draws per bucket to reuse the lines
-    return n * sizeof(Bucket) > (136ull << 20) && k * 8 >= n && nreg <= RS_MAX_REGIONS;
+    // table beyond ~116 MB (measured crossover on B200 with the round-2 region
+    // plan: direct / region 7.50 / 7.73 ms per 1e9 draws at 112 MB, 8.39 / 7.59
+    // at 128 MB, 9.28 / 7.55 at 144 MB) and enough draws per bucket to reuse
+    // the lines
+    return n * sizeof(Bucket) > (116ull << 20) && k * 8 >= n && nreg <= RS_MAX_REGIONS;
 }
 
 struct RegionPlan {
