@@ -50,7 +50,9 @@ inline uint64_t default_job_items(uint64_t n) {
     while (j < kJobBucketsMax && 2 * j <= n / kJobTarget) j *= 2;
     const uint64_t p = (n + j - 1) / j;
     const uint64_t waves = p / kK4Lanes, last = p % kK4Lanes;
-    if (waves >= 1 && last != 0 && last < kK4Lanes / 2)
+    // (jobs shorter than the 1024 cap: any partial last wave; measured at
+    // n = 1.2e7, 1.65 waves of J = 128: build 0.470 -> 0.437 ms with J = 212)
+    if (waves >= 1 && last != 0 && (j < kJobBucketsMax || last < kK4Lanes / 2))
         j = (n + waves * kK4Lanes - 1) / (waves * kK4Lanes);
     return j;
 }

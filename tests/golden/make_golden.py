@@ -178,7 +178,7 @@ def default_jobs(n: int) -> int:
         j *= 2
     lanes = 148 * 12 * 32  # K4a's resident jobs: stretch jobs when the last wave is < half full
     waves, last = divmod(-(-n // j), lanes)
-    if waves >= 1 and 0 < last < lanes // 2:
+    if waves >= 1 and last > 0 and (j < 1024 or last < lanes // 2):
         j = -(-n // (waves * lanes))
     return max(1, -(-n // j))
 

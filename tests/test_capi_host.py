@@ -82,15 +82,17 @@ def test_out_of_path_entry_points_are_stubbed():
 
 def test_default_job_count():
     # jobs of J = pow2_floor(n / 49152) items clamped to [32, 1024], stretched
-    # to fill whole K4a waves (148 * 12 * 32 = 56832 jobs each) when the last
-    # wave would be less than half full (engine.h default_job_items)
+    # to fill whole K4a waves (148 * 12 * 32 = 56832 jobs each) when jobs are
+    # below the 1024 cap, or the last wave would be less than half full
+    # (engine.h default_job_items)
     assert wrs.default_jobs(1) == 1
     assert wrs.default_jobs(32) == 1
     assert wrs.default_jobs(33) == 2
     assert wrs.default_jobs(10**6) == -(-10**6 // 32)            # < one wave
     assert wrs.default_jobs(1 << 22) == -(-(1 << 22) // 74)       # 1.15 waves of J = 64 -> 1
     assert wrs.default_jobs(1 << 24) == -(-(1 << 24) // 296)      # 1.15 waves of J = 256 -> 1
-    assert wrs.default_jobs(10**8) == -(-10**8 // 1024)           # last wave 72 % full: kept
+    assert wrs.default_jobs(12_000_000) == -(-12_000_000 // 212)  # 1.65 waves of J = 128 -> 1
+    assert wrs.default_jobs(10**8) == -(-10**8 // 1024)           # J = 1024, last wave 72 % full: kept
     assert wrs.default_jobs(125_000_000) == -(-125_000_000 // 1100)  # 2.15 waves -> 2
     assert wrs.default_jobs(1 << 28) == (1 << 28) // 1024         # 4.61 waves: kept
     assert wrs.default_jobs(1 << 30) == -(-(1 << 30) // 1050)     # 18.45 waves -> 18
