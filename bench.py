@@ -718,12 +718,14 @@ def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):
     k = args.k
     host_out = torch.empty(k, dtype=torch.int32, pin_memory=True)
     steps = max(1, min(args.steps, 5))
-    times = []
+    times, phases = [], []
     for i in range(1 + steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         W = wrs.Weights.from_array(host_w.numpy())
+        ta = time.perf_counter()
         S = wrs.Sampler.build(W, "psa", 1)
+        tb = time.perf_counter()
         S.draw_into(SEED, k, 1, host_out.data_ptr())
         checksum = int(host_out[-1])  # the step's result read on the host
         t1 = time.perf_counter()
@@ -731,7 +733,9 @@ def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):
         W.free()
         if i:
             times.append(t1 - t0)
+            phases.append((ta - t0, tb - ta, t1 - tb))
     sec = statistics.median(times)
+    ph = phases[times.index(sec)] if sec in times else phases[-1]
     if world > 1:
         import torch.distributed as dist
         tdev = "cuda" if dist.get_backend() == "nccl" else "cpu"
@@ -741,6 +745,8 @@ def e2e(args, wrs, torch, world, rank, lo, hi, n_total, k_total):
     return {"value": (n_total + k * world) / sec / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * k, "ms_per_step": sec * 1e3,
             "api": "wrs_weights_from_array + wrs_sampler_build(psa) + wrs_sampler_draw",
+            "phases_ms": {"weights_from_array_h2d": ph[0] * 1e3, "build": ph[1] * 1e3,
+                          "draw_d2h": ph[2] * 1e3},
             "checksum_last": checksum}
 
 
