@@ -618,3 +618,26 @@ def test_host_output_draws_span_several_copy_chunks(P):
         assert np.array_equal(host, dev.cpu().numpy().view(np.uint32)), n
         ref = P.sample_many(S.buckets(), S.bucket_mean, 31, 1_000_000, 3)
         assert np.array_equal(S.draw(31, 1_000_000, 3), ref)
+
+
+@pytest.mark.parametrize("n", [12_000_000, 16_777_216, 50_000_000])
+def test_wave_fit_default_jobs_tables_bit_exact(P, n):
+    """Default job counts folded into whole K4a waves (non-power-of-two jobs
+    of 212 / 296 / 880 items at these n) give the oracle's table at that P,
+    for uniform and power-law weights; every one of the three draws checked
+    on a window."""
+    import torch
+    P_ = wrs.default_jobs(n)
+    assert P_ < 56832 and -(-n // P_) not in (128, 256, 512)  # one wave of stretched jobs
+    for w in (P.generate_uniform(n, 3), P.generate_powerlaw(n, 0.5, 4)):
+        W, S = build(w)
+        assert S.jobs == P_
+        assert_same_table(S, w, P_, P)
+        k = 3_000_000
+        out = torch.empty(k, dtype=torch.int32, device="cuda")
+        S.draw_device(11, k, 1, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32),
+                              P.sample_many(S.buckets(), S.bucket_mean, 11, k, 1))
+        S.free()
+        W.free()
