@@ -384,11 +384,14 @@ constexpr int RC_SPAN = RC_ROWS * 256;  // slab positions per gather / count CTA
 #ifndef RS_MIN_CTAS
 #define RS_MIN_CTAS 6  // 256-thread CTAs per SM the register budget must allow (40 regs; 8.05 vs 8.16 ms at 5)
 #endif
+#ifndef RS32_SM_THREADS
+#define RS32_SM_THREADS 1024  // 32-row scatter threads per SM the registers must allow (64 each)
+#endif
 // ROWS: draws per thread (tile = TT * ROWS); 32 rows keep 256-thread CTAs
 // for 8192-draw tiles (4 CTAs per SM: 64 registers for the 32 buckets).
 template <bool W1, bool ORDER = true, bool PHX = false, int TT = RS_THREADS, bool FULL = false,
           int ROWS = RS_ROWS>
-__global__ void __launch_bounds__(TT, (ROWS == RS_ROWS ? RS_MIN_CTAS * 256 : ROWS == 32 ? 1024 : 512) / TT)
+__global__ void __launch_bounds__(TT, (ROWS == RS_ROWS ? RS_MIN_CTAS * 256 : ROWS == 32 ? RS32_SM_THREADS : 512) / TT)
 k_region_scatter(RegionGeom rg, uint32_t tile0, uint32_t* __restrict__ cursor,
                  unsigned* __restrict__ overflow, void* __restrict__ rec_out,
                  uint16_t* __restrict__ slot_of, RunInfo* __restrict__ runs) {
