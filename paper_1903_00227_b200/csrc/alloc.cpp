@@ -6,7 +6,10 @@
 // a loop (the reference's usage, and the e2e benchmark) would pay that every
 // time.  Freed blocks are kept per (device, size) and handed out again for an
 // allocation of exactly that size.  A block is cached only after the device
-// is idle (cudaDeviceSynchronize), so no in-flight work can still touch it.
+// is idle (cudaDeviceSynchronize), so no in-flight work can still touch it --
+// unless the caller holds an armed SyncedFrees (engine.h): it has synchronised
+// every stream that used the block, and the device-wide wait would only stall
+// this thread behind other threads' work.
 // Cached bytes are capped (WRS_B200_CACHE_MB, default 8 GB per process);
 // an allocation that fails for lack of memory returns every cached block of
 // its device and retries, and wrs_b200_release_cache() hands every cached
@@ -82,6 +85,21 @@ cudaError_t dev_malloc(void** p, size_t bytes) {
     return e;
 }
 
+namespace {
+thread_local int t_synced_frees = 0;
+}
+
+void SyncedFrees::arm() {
+    if (!armed) {
+        armed = true;
+        ++t_synced_frees;
+    }
+}
+
+SyncedFrees::~SyncedFrees() {
+    if (armed) --t_synced_frees;
+}
+
 void dev_free(void* p) {
     if (!p) return;
     Cache& c = cache();
@@ -96,7 +114,8 @@ void dev_free(void* p) {
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != key.first) cudaSetDevice(key.first);
-    if (c.cached + key.second <= c.limit && cudaDeviceSynchronize() == cudaSuccess) {
+    if (c.cached + key.second <= c.limit &&
+        (t_synced_frees > 0 || cudaDeviceSynchronize() == cudaSuccess)) {
         c.free_blocks.insert({key, p});
         c.cached += key.second;
     } else {

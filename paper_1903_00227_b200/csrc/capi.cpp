@@ -123,6 +123,15 @@ struct WeightsData {
     bool owned = true;
     double total = 0.0;
     std::unique_ptr<DevBuf> storage;
+    // set when the values were written or read by work this library did not
+    // synchronise itself (device-to-device copies, caller-stream rebuilds):
+    // freeing them then waits for the whole device
+    std::atomic<bool> ext{false};
+    ~WeightsData() {
+        wrsb::SyncedFrees synced;
+        if (!ext.load()) synced.arm();
+        storage.reset();
+    }
     mutable std::mutex host_mu;
     mutable std::vector<double> host;  // lazily materialised values()
     mutable bool host_ready = false;
@@ -146,6 +155,7 @@ void finalize_weights(WeightsData& wd, const std::string& file_for_format_error)
     if (wd.n == 0) throw std::invalid_argument("weights: need at least one item");
     wrsb::Workspace ws;
     ck(wrsb::workspace_alloc_total(ws, wd.n), "workspace");
+    wrsb::SyncedFrees synced;  // destroyed after guard: covers its frees
     struct Guard {
         wrsb::Workspace& w;
         ~Guard() { wrsb::workspace_free(w); }
@@ -155,6 +165,7 @@ void finalize_weights(WeightsData& wd, const std::string& file_for_format_error)
     wrsb::DevScalars sc{};
     ck(cudaMemcpyAsync(&sc, ws.sc, sizeof sc, cudaMemcpyDeviceToHost, st.s), "scalars D2H");
     ck(cudaStreamSynchronize(st.s), "K0");
+    synced.arm();
     if (sc.bad_index != ~0ull) {
         if (!file_for_format_error.empty())
             throw format_error("weight " + std::to_string(sc.bad_index) +
@@ -173,7 +184,15 @@ std::shared_ptr<WeightsData> weights_from_host(const double* w, uint64_t n,
     if (n == 0) throw std::invalid_argument("weights: need at least one item");
     wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
     wd->d_w = static_cast<double*>(wd->storage->p);
-    ck(cudaMemcpy(wd->d_w, w, n * sizeof(double), cudaMemcpyHostToDevice), "weights H2D");
+    {
+        // on a non-blocking stream, not the legacy one: a synchronous legacy
+        // copy was measured waiting behind another host thread's draw
+        // downloads, while PCIe carries both directions at once
+        Stream st;
+        ck(cudaMemcpyAsync(wd->d_w, w, n * sizeof(double), cudaMemcpyHostToDevice, st.s),
+           "weights H2D");
+        ck(cudaStreamSynchronize(st.s), "weights H2D");
+    }
     finalize_weights(*wd, file);
     return wd;
 }
@@ -280,6 +299,10 @@ struct wrs_sampler {
     bool keep_ws = false;
     cudaEvent_t ev[8] = {};
     bool timed = false;
+    // set once any call ran this sampler's work on a caller's stream: the
+    // destructor then cannot know when that work ends and frees with a
+    // device-wide wait (otherwise it synchronises its own streams only)
+    mutable std::atomic<bool> ext_stream{false};
     std::mutex mu;  // rebuild / stage access
     // draw scratch (region plan), reused across draws; sws_ev orders users
     mutable wrsb::SampleWorkspace sws;
@@ -297,6 +320,15 @@ struct wrs_sampler {
 
     ~wrs_sampler() {
         if (device >= 0) cudaSetDevice(device);
+        wrsb::SyncedFrees synced;
+        if (!ext_stream.load()) {
+            bool ok = true;
+            for (Stream* st : {stream.get(), side.get(), hi.get()})
+                if (st) ok = ok && cudaStreamSynchronize(st->s) == cudaSuccess;
+            if (ok) synced.arm();
+        } else if (weights) {
+            weights->ext = true;
+        }
         wrsb::workspace_free(ws);
         if (sws_ev) cudaEventSynchronize(sws_ev), cudaEventDestroy(sws_ev);
         if (side_ev) cudaEventSynchronize(side_ev), cudaEventDestroy(side_ev);
@@ -312,6 +344,9 @@ struct wrs_sampler {
             if (built_ev[b]) cudaEventSynchronize(built_ev[b]), cudaEventDestroy(built_ev[b]);
             if (read_ev[b]) cudaEventSynchronize(read_ev[b]), cudaEventDestroy(read_ev[b]);
         }
+        buckets.reset();  // inside the SyncedFrees scope
+        buckets2.reset();
+        weights.reset();
     }
     // Double-buffered tables (wrs_b200_sampler_double_buffer): rebuilds write
     // the back table while draws already issued still read the front one;
@@ -331,6 +366,14 @@ struct wrs_sampler {
 };
 
 namespace {
+
+// The stream a call runs on: the caller's (marking the sampler, see
+// ext_stream) or the sampler's own.
+cudaStream_t use_stream(const wrs_sampler& s, void* stream) {
+    if (!stream) return s.stream->s;
+    s.ext_stream = true;
+    return static_cast<cudaStream_t>(stream);
+}
 
 void read_scalars(wrs_sampler& s) {
     wrsb::DevScalars sc{};
@@ -361,7 +404,11 @@ std::unique_ptr<wrs_sampler> build_psa(const std::shared_ptr<WeightsData>& wd, u
                               nullptr),
        "PSA launch");
     read_scalars(*s);
-    if (!s->keep_ws) wrsb::workspace_free(s->ws);
+    if (!s->keep_ws) {
+        wrsb::SyncedFrees synced;  // read_scalars synchronised the build stream
+        synced.arm();
+        wrsb::workspace_free(s->ws);
+    }
     return s;
 }
 
@@ -439,6 +486,7 @@ void draw_to_host(const wrs_sampler& s, uint64_t seed, uint64_t count, unsigned 
     // starts after one small chunk's draw instead of a 2^28-draw one; the
     // extra table sweeps stay hidden under the copies
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 26);
+    wrsb::SyncedFrees synced;  // armed once both streams are drained
     DevBuf b0(chunk * 4), b1(chunk * 4);
     uint32_t* bufs[2] = {static_cast<uint32_t*>(b0.p), static_cast<uint32_t*>(b1.p)};
     Stream copy;
@@ -470,6 +518,7 @@ void draw_to_host(const wrs_sampler& s, uint64_t seed, uint64_t count, unsigned 
     }
     ck(cudaStreamSynchronize(copy.s), "draw");
     ck(cudaStreamSynchronize(s.stream->s), "draw");
+    synced.arm();
 }
 
 void draw_counts(const wrs_sampler& s, uint64_t seed, uint64_t k, unsigned workers,
@@ -781,6 +830,7 @@ wrs_status wrs_b200_weights_from_device(const double* d_w, uint64_t n, int copy,
             wd->storage = std::make_unique<DevBuf>(n * sizeof(double));
             wd->d_w = static_cast<double*>(wd->storage->p);
             ck(cudaMemcpy(wd->d_w, d_w, n * sizeof(double), cudaMemcpyDeviceToDevice), "D2D");
+            wd->ext = true;  // legacy-stream copy, not synchronised here
         } else {
             wd->d_w = const_cast<double*>(d_w);
             wd->owned = false;
@@ -815,6 +865,8 @@ wrs_status wrs_b200_weights_generate_range(const char* dist, double param, uint6
             ck(cudaMemcpy(wd->d_w, full->d_w + lo, wd->n * sizeof(double),
                           cudaMemcpyDeviceToDevice),
                "slice");
+            wd->ext = true;  // legacy-stream copy, not synchronised here
+            full->ext = true;
             finalize_weights(*wd, "");
             *out = new wrs_weights{wd};
             return WRS_OK;
@@ -881,7 +933,7 @@ wrs_status wrs_b200_sampler_rebuild_async(wrs_sampler* s, void* stream) {
         std::lock_guard<std::mutex> g(s->mu);
         ck(cudaSetDevice(s->device), "cudaSetDevice");
         if (!s->ws.sc) ck(wrsb::workspace_alloc(s->ws, s->n, s->P, false), "workspace");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        cudaStream_t st = use_stream(*s, stream);
         s->timed = g_timing.load() != 0;
         if (s->timed && !s->ev[0])
             for (cudaEvent_t& e : s->ev) ck(cudaEventCreate(&e), "event");
@@ -980,7 +1032,7 @@ wrs_status wrs_b200_sampler_draw_device(const wrs_sampler* s, uint64_t seed, uin
     if (!s || (!d_out && count)) return fail(WRS_EINVAL, "null argument");
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        cudaStream_t st = use_stream(*s, stream);
         sample_on(*s, seed, 0, count, count, workers ? workers : 1, 0, d_out, st);
         return WRS_OK;
     });
@@ -991,7 +1043,7 @@ wrs_status wrs_b200_sampler_draw_philox_device(const wrs_sampler* s, uint64_t se
     if (!s || (!d_out && count)) return fail(WRS_EINVAL, "null argument");
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        cudaStream_t st = use_stream(*s, stream);
         sample_on(*s, seed, 0, count, count, 1, 0, d_out, st, wrsb::kPhiloxStream);
         return WRS_OK;
     });
@@ -1015,7 +1067,7 @@ wrs_status wrs_b200_sampler_draw_counts_device(const wrs_sampler* s, uint64_t se
     if (!s || !d_items || !d_counts || !d_n_unique) return fail(WRS_EINVAL, "null argument");
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        cudaStream_t st = use_stream(*s, stream);
         count_on(*s, seed, k, workers ? workers : 1, d_items, d_counts, d_n_unique, st);
         return WRS_OK;
     });
@@ -1097,7 +1149,7 @@ wrs_status wrs_b200_sampler_draw_shard_device(const wrs_sampler* s, uint64_t see
     if (base + s->n > (uint64_t{1} << 32)) return fail(WRS_EINVAL, "global ids exceed 2^32");
     return guarded([&] {
         ck(cudaSetDevice(s->device), "cudaSetDevice");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream->s;
+        cudaStream_t st = use_stream(*s, stream);
         sample_on(*s, wrs_b200_shard_seed(seed, shard), 0, count, count, 1,
                   static_cast<uint32_t>(base), d_out, st);
         return WRS_OK;
@@ -1382,7 +1434,7 @@ wrs_status wrs_b200_multi_exchange(wrs_b200_multi* m, void* stream) {
     return guarded([&] {
         if (!m->comm) throw std::invalid_argument("handle has no NCCL communicator");
         ck(cudaSetDevice(m->device), "cudaSetDevice");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : m->shard->stream->s;
+        cudaStream_t st = use_stream(*m->shard, stream);
         nck(need_nccl().allGather(m->d_total->p, m->d_totals->p, 1, ncclFloat64, m->comm, st),
             "ncclAllGather");
         multi_read_totals(*m, st);

@@ -23,6 +23,15 @@ void poison(void* p, size_t bytes, cudaStream_t st);
 // Caching device allocator for the library's large buffers (alloc.cpp).
 cudaError_t dev_malloc(void** p, size_t bytes);
 void dev_free(void* p);
+// While an armed SyncedFrees is in scope on this thread, dev_free skips its
+// device-wide synchronise: the caller has already synchronised every stream
+// that used the buffers it frees (so a free on one host thread no longer
+// waits for another thread's copies and kernels on other streams).
+struct SyncedFrees {
+    bool armed = false;
+    void arm();
+    ~SyncedFrees();
+};
 // Returns every cached block to the driver; the bytes released.
 size_t release_cache();
 

@@ -641,3 +641,60 @@ def test_wave_fit_default_jobs_tables_bit_exact(P, n):
                               P.sample_many(S.buckets(), S.bucket_mean, 11, k, 1))
         S.free()
         W.free()
+
+
+def test_concurrent_host_threads_build_draw_free(P):
+    """Host threads each running upload -> build -> draw into host memory ->
+    free through the ABI at once (the e2e bench's two lanes): a free waits
+    for its own sampler's streams only (SyncedFrees, alloc.cpp), so a block
+    another thread gets back from the cache must hold no in-flight work.
+    Every draw equals the same job run alone."""
+    import threading
+    k = (1 << 26) + 4_321  # two copy chunks
+    cases = [(P.generate_uniform(2_000_003 + 7 * j, 40 + j), 50 + j) for j in range(3)]
+    want = []
+    for w, seed in cases:
+        W, S = build(w)
+        want.append(S.draw(seed, k, 2))
+        S.free()
+        W.free()
+    bad = []
+
+    def lane(j):
+        w, seed = cases[j]
+        for _ in range(4):
+            W, S = build(w)
+            got = S.draw(seed, k, 2)
+            S.free()
+            W.free()
+            if not np.array_equal(got, want[j]):
+                bad.append(j)
+
+    ths = [threading.Thread(target=lane, args=(j,)) for j in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not bad
+
+
+def test_free_after_draw_on_caller_stream_waits_for_it(P):
+    """A sampler whose draw ran on the caller's stream is freed without
+    synchronising that stream: the free must still wait for the draw
+    (ext_stream -> device-wide wait) before its table goes back to the cache
+    and the next sampler of the same size overwrites it."""
+    import torch
+    n, k = 3_000_017, 1 << 27
+    w1, w2 = P.generate_uniform(n, 61), P.generate_powerlaw(n, 1.0, 62)
+    W, S = build(w1)
+    want = S.draw(63, 1 << 20, 1)
+    out = torch.empty(k, dtype=torch.int32, device="cuda")
+    st = torch.cuda.Stream()
+    S.draw_device(63, k, 1, out, stream=st.cuda_stream)
+    S.free()
+    W.free()
+    W2, S2 = build(w2)  # same sizes: reuses the freed blocks
+    torch.cuda.synchronize()
+    assert np.array_equal(out[: 1 << 20].cpu().numpy().view(np.uint32), want)
+    S2.free()
+    W2.free()
