@@ -765,20 +765,21 @@ def e2e_lanes(wrs, torch, host_w, k, steps, checksum):
     with the other lane's downloads.  Every step's last draw is checked
     against the serial run's (same seed, same weights)."""
     import threading
-    per_lane = max(2, steps)
+    per_lane = [2, max(8, steps)]  # warm-up round, timed round (8: the start-up
+    # upload and the drain of the last download spread over 16 steps)
     outs = [torch.empty(k, dtype=torch.int32, pin_memory=True) for _ in range(2)]
     start = threading.Barrier(2)
     uploaded = threading.Event()
     lane_ms = [[], []]
     errors = []
 
-    def lane(j):
+    def lane(j, steps):
         try:
             out = outs[j]
             start.wait()
             if j:
                 uploaded.wait()
-            for _ in range(per_lane):
+            for _ in range(steps):
                 t = [time.perf_counter()]
                 W = wrs.Weights.from_array(host_w.numpy())
                 uploaded.set()
@@ -800,7 +801,7 @@ def e2e_lanes(wrs, torch, host_w, k, steps, checksum):
 
     # one untimed round to warm both lanes' allocations
     for timed in (False, True):
-        ths = [threading.Thread(target=lane, args=(j,)) for j in range(2)]
+        ths = [threading.Thread(target=lane, args=(j, per_lane[timed])) for j in range(2)]
         uploaded.clear()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -814,7 +815,7 @@ def e2e_lanes(wrs, torch, host_w, k, steps, checksum):
         if not timed:
             for ms in lane_ms:
                 ms.clear()
-    return (t1 - t0) / (2 * per_lane), lane_ms
+    return (t1 - t0) / (2 * per_lane[1]), lane_ms
 
 
 if __name__ == "__main__":
